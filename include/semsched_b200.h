@@ -1,0 +1,244 @@
+/*
+ * semsched_b200.h — C-ABI of the B200-native semantic-scheduling hot path.
+ *
+ * Drop-in boundary for the reference's simulation entry points
+ * (reference = arXiv 2506.12204 package `semsched`, paths relative to
+ * /root/reference/pkg/src/semsched):
+ *
+ *   ss_run_traces / ss_run_traces_host
+ *       replace `run(cfg, arrivals) -> Trace`           engine.py:444-450
+ *       and `Simulator(cfg).run(arrivals)`               engine.py:152-243
+ *       batched over many independent traces (the reference runs one
+ *       trace per call; `sweeps.sweep` loops them, sweeps.py:25-47).
+ *       One call runs every scheduler round of every trace:
+ *         per round  `Simulator._schedule`              engine.py:246-254
+ *                    -> `stage_aware_schedule`          batching.py:57-88
+ *                    `Simulator._execute`               engine.py:288-380
+ *                    -> `priority_based_eviction`       kvcache.py:137-179
+ *                    -> `should_recompute`              kvcache.py:81-134
+ *   ss_trace_stats (output) replaces the waiting-time statistics of
+ *       `metrics.average_waiting_time` / `normalized_waiting_time` /
+ *       `overall_normalized_waiting_time`               metrics.py:35-56
+ *
+ * Every entry point takes plain pointers and sizes; no torch types.
+ * Inputs are structure-of-arrays, all traces concatenated, each trace's
+ * requests in the reference's *pending* order, i.e. sorted by
+ * (prediction-ready time, arrival time, id)        predictors.py:148.
+ *
+ * Error behaviour mirrors the reference: invalid arguments -> SS_ERR_INVALID_ARG
+ * (reference: ValueError, engine.py:102-108); unservable requests are
+ * RETURNED (never raised), exactly like Trace.unservable (engine.py:82).
+ * A trace whose state stops changing (the reference would spin forever in
+ * engine.py:202-224) reports SS_TRACE_LIVELOCK instead.
+ */
+#ifndef SEMSCHED_B200_H
+#define SEMSCHED_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define SS_OK                 0
+#define SS_ERR_INVALID_ARG    1  /* reference: ValueError / ConfigError       */
+#define SS_ERR_CUDA           2  /* CUDA runtime failure (message via ss_last_error) */
+#define SS_ERR_TRACE_FAILED   3  /* >=1 trace ended with a non-OK trace status */
+#define SS_ERR_NO_DEVICE      4  /* no CUDA device: there is no CPU fallback   */
+#define SS_ERR_UNSUPPORTED    5  /* configuration outside the kernel's limits  */
+
+/* ---- per-trace status (ss_trace_stats.status) --------------------------- */
+#define SS_TRACE_OK           0
+#define SS_TRACE_LIVELOCK     1  /* round made no progress and state repeats    */
+#define SS_TRACE_ROUND_CAP    2  /* params.max_rounds reached                    */
+#define SS_TRACE_LOG_OVERFLOW 3  /* round log region too small                   */
+#define SS_TRACE_INTERNAL     4  /* invariant violated (allocation > free, ...)  */
+
+/* ---- policies (engine.py:40-44, keys engine.py:114-123) ---------------- */
+#define SS_POLICY_SEMANTIC 0
+#define SS_POLICY_FCFS     1
+#define SS_POLICY_SJF      2
+#define SS_POLICY_HPJF     3
+
+/* ---- flags ----------------------------------------------------------- */
+#define SS_FLAG_ROUND_LOG  1u   /* write per-round ITERATION_END records     */
+#define SS_FLAG_DIGEST     2u   /* accumulate the per-trace schedule digest   */
+
+/* limits of the device path */
+#define SS_MAX_BATCH       32   /* one scheduler candidate per lane of a warp */
+#define SS_MAX_LEVELS      16   /* true-urgency levels in ss_trace_stats      */
+#define SS_MAX_TRACE_REQS  (1u << 24)  /* tie rank packs into 24 bits        */
+
+/* Analytical cost profile, costs.py:21-41 (GpuProfile). */
+typedef struct ss_profile {
+    double alpha1, alpha2;   /* prefill(n)  = alpha1*n*n + alpha2*n          */
+    double gamma1, gamma2;   /* decode step = gamma1*(n+j-1) + gamma2        */
+    double beta_load;        /* reload(k)   = beta_load*k                     */
+    double beta_save;        /* carried for API completeness (unused by ref) */
+} ss_profile;
+
+/* ScenarioConfig knobs the hot path reads (engine.py:89-111). */
+typedef struct ss_params {
+    ss_profile profile;
+    int64_t memory_capacity;   /* token slots, DeviceMemory.capacity          */
+    int32_t batch_size;        /* b, 1..SS_MAX_BATCH                          */
+    int32_t policy;            /* SS_POLICY_*                                 */
+    int32_t dependency_rule;   /* kvcache.py:111                              */
+    int32_t decode_cost_sum;   /* 0: "max", 1: "sum"   (engine.py:148)        */
+    int32_t levels;            /* true-urgency levels for the stats (<=16)    */
+    uint32_t flags;            /* SS_FLAG_*                                    */
+    int64_t max_rounds;        /* per-trace round cap, 0 = unlimited          */
+} ss_params;
+
+/* Requests of all traces, concatenated; trace t owns
+ * [trace_offsets[t], trace_offsets[t+1]), in pending order. */
+typedef struct ss_trace_batch {
+    int32_t  n_traces;
+    int32_t  _pad;
+    int64_t  n_requests;
+    const int64_t*  trace_offsets;    /* [n_traces+1]                            */
+    const double*   ready_time;       /* prediction_ready_time                   */
+    const double*   arrival_time;     /* Request.arrival_time                    */
+    const uint32_t* prompt_len;       /* Request.prompt_len (>=1)                */
+    const uint32_t* true_output_len;  /* Request.true_output_len (>=1)           */
+    const uint32_t* pred_len;         /* predicted_bucket.representative_len     */
+    const uint8_t*  pred_urgency;     /* f_e.rank (dispatch key)                 */
+    const uint8_t*  true_urgency;     /* true_urgency.rank (stats only)          */
+    const uint32_t* tie_rank;         /* rank of (arrival_time, id) in the trace */
+} ss_trace_batch;
+
+/* Per-trace result record (fixed size, gathered across ranks). */
+typedef struct ss_trace_stats {
+    uint64_t digest;           /* schedule digest (SS_FLAG_DIGEST)                 */
+    int64_t  rounds;           /* _schedule+_execute rounds = scheduler decisions  */
+    int64_t  evictions;        /* Trace.eviction_count                             */
+    int64_t  mem_used_peak;    /* max ITERATION_END mem_used                       */
+    int64_t  log_words;        /* words written to the round log                   */
+    int32_t  completed;
+    int32_t  unservable;       /* len(Trace.unservable)                            */
+    int32_t  status;           /* SS_TRACE_*                                       */
+    int32_t  lost_evictions;   /* evictions made by an admission that then failed:
+                                  applied but, as in the reference, not recorded   */
+    int32_t  anomalies;        /* granted while still queued    */
+    int32_t  _pad;
+    double   final_clock;      /* RUN_END time                                     */
+    /* CPython-3.12 float sum() (Neumaier) over completed records in trace order  */
+    double   sum_wait;         /* sum(finish - arrival)                            */
+    double   sum_norm_wait;    /* sum((finish - arrival)/generated)                */
+    double   level_norm_sum[SS_MAX_LEVELS];
+    int32_t  level_count[SS_MAX_LEVELS];
+} ss_trace_stats;
+
+/* Per-request outputs, same indexing as the inputs. NaN encodes None. */
+typedef struct ss_request_out {
+    double*   first_scheduled;  /* RequestRecord.first_scheduled  */
+    double*   finish_time;      /* RequestRecord.finish_time      */
+    uint32_t* generated;        /* RequestRecord.generated_tokens */
+    uint32_t* evictions;        /* RequestRecord.evictions        */
+    double*   f_t;              /* final Request.f_t  (optional, may be NULL)      */
+    uint32_t* state;            /* final stage | prefilled<<8 (optional, NULL ok)  */
+} ss_request_out;
+
+/* Whole-call outputs. */
+typedef struct ss_outputs {
+    ss_request_out req;
+    ss_trace_stats* stats;          /* [n_traces]                                  */
+    uint32_t* unservable_slots;     /* [n_requests]: trace t's list starts at
+                                       trace_offsets[t]; slots are trace-local     */
+    uint32_t* round_log;            /* SS_FLAG_ROUND_LOG: words                    */
+    const int64_t* log_offsets;     /* [n_traces+1] word ranges into round_log     */
+} ss_outputs;
+
+/* Stage encoding of ss_request_out.state (requests.py:17-23). */
+#define SS_STAGE_WAITING    0
+#define SS_STAGE_DECODING   2
+#define SS_STAGE_COMPLETED  5
+#define SS_STAGE_UNSERVABLE 6   /* removed by _mark_unservable (engine.py:402-412) */
+
+/* ---- round log record (one per ITERATION_END event, engine.py:329-380) ----
+ * word 0 kind (0 decode, 1 prefill, 2 nothing granted), 1 m granted,
+ * 2 c completed, 3 v decisions, 4-5 mem_used (u64), 6-7 time (f64 bits),
+ * then v decisions of SS_LOG_DECISION_WORDS words each (in eviction order):
+ *   victim slot, action (0 offload, 1 discard), decode_saved, decode_discarded,
+ *   freed_slots, f_t_before (2 words), f_t_after (2 words),
+ * then m granted slots (batch order), then c completed slots (granted order).
+ * Slots are trace-local pending-order row indices.
+ */
+#define SS_LOG_HEADER_WORDS    8
+#define SS_LOG_DECISION_WORDS  9
+#define SS_KIND_DECODE   0
+#define SS_KIND_PREFILL  1
+#define SS_KIND_NONE     2
+
+/* ---- schedule digest -------------------------------------------------
+ * Order-sensitive and lane-parallel: a sum (mod 2^64) of one hashed term per
+ * (round, field, position). Shared verbatim by the oracle (tests) and the
+ * device so full-size parity reduces to comparing one u64 per trace. */
+#if defined(__CUDACC__)
+#define SS_HD __host__ __device__ __forceinline__
+#else
+#define SS_HD static inline
+#endif
+SS_HD uint64_t ss_mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+SS_HD uint64_t ss_term(uint64_t round, uint32_t tag, uint32_t idx, uint64_t v) {
+    return ss_mix64(ss_mix64((round << 24) ^ ((uint64_t)tag << 20) ^ (uint64_t)idx) ^ v);
+}
+#define SS_TAG_HDR   1u
+#define SS_TAG_MEM   2u
+#define SS_TAG_TIME  3u
+#define SS_TAG_GRANT 4u
+#define SS_TAG_DONE  5u
+#define SS_TAG_EV0   6u   /* victim | action<<32     */
+#define SS_TAG_EV1   7u   /* saved | discarded<<32   */
+#define SS_TAG_EV2   8u   /* freed                   */
+#define SS_TAG_EV3   9u   /* f_t_before bits         */
+#define SS_TAG_EV4  10u   /* f_t_after bits          */
+SS_HD uint64_t ss_hdr_word(uint32_t kind, uint32_t m, uint32_t c, uint32_t v) {
+    return (uint64_t)kind | ((uint64_t)m << 8) | ((uint64_t)c << 24) | ((uint64_t)v << 40);
+}
+
+/* ---- entry points ----------------------------------------------------- */
+
+/* Last error message of the calling thread ("" if none). */
+const char* ss_last_error(void);
+
+/* Library / device info. Returns SS_OK, or SS_ERR_NO_DEVICE. */
+int ss_device_info(int* device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* Device workspace the run needs (bytes), for callers that pre-allocate. */
+int ss_workspace_bytes(const ss_params* params, int32_t n_traces, int64_t n_requests,
+                       size_t* bytes);
+
+/* Run every trace to completion. All pointers in `batch` and `out` are DEVICE
+ * pointers; `workspace` is a device buffer of >= ss_workspace_bytes bytes
+ * (NULL: the library allocates and frees one). `stream` is a cudaStream_t
+ * (NULL = legacy default stream). Asynchronous w.r.t. the host unless the
+ * library allocated the workspace. `kernel_ms` (nullable) receives the
+ * scheduler kernel's device time measured with events on `stream`
+ * (forces a sync). Returns SS_OK, SS_ERR_TRACE_FAILED (see stats[].status),
+ * or an error. */
+int ss_run_traces(const ss_params* params, const ss_trace_batch* batch,
+                  const ss_outputs* out, void* workspace, size_t workspace_bytes,
+                  void* stream, float* kernel_ms);
+
+/* Same, with every pointer in `batch` and `out` on the HOST (pinned or
+ * pageable). Copies in, runs, copies out, synchronises. This is the
+ * reference-facing plugin call (host buffers in, host buffers out). */
+int ss_run_traces_host(const ss_params* params, const ss_trace_batch* batch,
+                       const ss_outputs* out, void* stream, float* kernel_ms);
+
+/* Number of warps the scheduler kernel keeps resident (for reporting). */
+int ss_kernel_config(const ss_params* params, int32_t n_traces, int* blocks,
+                     int* warps_per_block, int* smem_bytes_per_block);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEMSCHED_B200_H */
