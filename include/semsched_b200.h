@@ -55,6 +55,9 @@ extern "C" {
 #define SS_TRACE_ROUND_CAP    2  /* params.max_rounds reached                    */
 #define SS_TRACE_LOG_OVERFLOW 3  /* round log region too small                   */
 #define SS_TRACE_INTERNAL     4  /* invariant violated (allocation > free, ...)  */
+#define SS_TRACE_ANOMALY      5  /* a request was granted while still queued: the
+                                    reference keeps a stale heap entry for it
+                                    (DESIGN.md §5); not emulated                 */
 
 /* ---- policies (engine.py:40-44, keys engine.py:114-123) ---------------- */
 #define SS_POLICY_SEMANTIC 0

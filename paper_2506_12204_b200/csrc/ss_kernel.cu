@@ -1,0 +1,1126 @@
+// ss_kernel.cu — warp-per-trace semantic scheduler for sm_100a.
+//
+// One warp owns one arrival trace and runs every scheduler round of it
+// (the reference's Simulator.run loop, engine.py:202-224) without leaving the
+// SM. Traces are independent, so warps pull trace ids from a global counter
+// (persistent, load-balanced); 4,096 traces keep ~28 warps resident per SM.
+//
+// Per-trace state:
+//   * dispatch queue = sorted FRONT (64 packed keys, shared memory) + unsorted
+//     BACK (HBM); every BACK key is larger than every FRONT key, so the
+//     top-b candidates are FRONT[0..b) and the dual heap of heaps.py:32-237
+//     becomes a merge-by-rank in shared memory. The BACK is refilled with a
+//     warp bitonic top-32 selection when the FRONT runs short.
+//   * ongoing batch (engine.py:165) lives in registers: lane i = member i.
+//   * resident set (the eviction heap, heaps.py:174-207) is an unsorted HBM
+//     list scanned with a warp arg-max only when memory is short.
+//   * per-request dynamic state (f_t, decoded, stage bits) is SoA in HBM.
+//
+// Packed dispatch key (requests.py:81-91, engine.py:114-123), 96 bits:
+//   hi = rank:8 | f_t bits 62..7        lo = f_t bits 6..0 | tie:25
+// f_t > 0 for every live request, so its IEEE bits order like the value;
+// tie = rank of (arrival, id) inside the trace. The order is total, which
+// makes heap shape irrelevant: any exact top-b reproduces the heap's pops.
+//
+// All float64 arithmetic goes through ss_costs.cuh in the reference's
+// association order with explicit round-to-nearest intrinsics (no FMA).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ss_costs.cuh"
+#include "ss_kernel.cuh"
+
+namespace ss {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint32_t ST_WAIT = 0, ST_DEC = 2, ST_DONE = 5, ST_UNS = 6;
+constexpr uint32_t F_STAGE = 7u, F_PF = 8u, F_Q = 16u, F_INS = 32u, F_FIRST = 64u, F_GRANT = 128u;
+constexpr uint32_t SLOT_MASK = 0x00FFFFFFu, DEC_BIT = 0x80000000u;
+
+struct __align__(16) Key {
+    unsigned long long hi;
+    uint32_t lo;
+    uint32_t aux;  // slot | decoding << 31
+};
+
+struct __align__(16) MemS {
+    double ft;
+    uint32_t slot, prompt, tout, mid;
+    uint32_t urank, tie, dec, flg;
+};
+
+struct WarpSmem {
+    Key F[FCAP];    // sorted queue front
+    Key X[32];      // scratch keys (ongoing keys / insert ranking / refill)
+    MemS M[32];     // member hand-off between lanes
+};
+
+__device__ __forceinline__ bool klt(const Key& a, const Key& b) {
+    return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo);
+}
+__device__ __forceinline__ Key kinf() {
+    Key k;
+    k.hi = ~0ull;
+    k.lo = ~0u;
+    k.aux = ~0u;
+    return k;
+}
+__device__ __forceinline__ Key kshfl(const Key& k, int src) {
+    Key r;
+    r.hi = __shfl_sync(FULL, k.hi, src);
+    r.lo = __shfl_sync(FULL, k.lo, src);
+    r.aux = __shfl_sync(FULL, k.aux, src);
+    return r;
+}
+__device__ __forceinline__ Key kshfl_xor(const Key& k, int m) {
+    Key r;
+    r.hi = __shfl_xor_sync(FULL, k.hi, m);
+    r.lo = __shfl_xor_sync(FULL, k.lo, m);
+    r.aux = __shfl_xor_sync(FULL, k.aux, m);
+    return r;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ long long warp_incl_scan_ll(long long v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long t = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+template <int POL>
+__device__ __forceinline__ Key make_key(uint32_t urank, double ft, uint32_t tie, uint32_t slot,
+                                        bool decoding) {
+    unsigned long long fb = (unsigned long long)__double_as_longlong(ft);
+    Key k;
+    if (POL == SS_POLICY_SEMANTIC) {
+        k.hi = ((unsigned long long)urank << 56) | (fb >> 7);
+        k.lo = ((uint32_t)(fb & 127ull) << 25) | tie;
+    } else if (POL == SS_POLICY_FCFS) {
+        k.hi = 0ull;
+        k.lo = tie;
+    } else if (POL == SS_POLICY_SJF) {
+        k.hi = fb >> 7;
+        k.lo = ((uint32_t)(fb & 127ull) << 25) | tie;
+    } else {
+        k.hi = (unsigned long long)urank << 56;
+        k.lo = tie;
+    }
+    k.aux = slot | (decoding ? DEC_BIT : 0u);
+    return k;
+}
+
+__device__ __forceinline__ Key* BK(const KArgs& A) { return reinterpret_cast<Key*>(A.w.B); }
+
+__device__ __forceinline__ unsigned long long dbits(double x) {
+    return (unsigned long long)__double_as_longlong(x);
+}
+
+// --------------------------------------------------------------------------
+// trace context (warp-uniform)
+// --------------------------------------------------------------------------
+struct Trace {
+    long long off;
+    int n, npend, cursor;
+    double clock;
+    long long used, cap;
+    int nF, nB, nR, nO, nins;
+    long long rounds, evictions, peak;
+    int status, nuns, lost, anomalies;
+    long long logpos, logcap;
+    uint32_t* log;
+};
+
+struct Env {
+    const KArgs* A;
+    WarpSmem* sm;
+    int lane;
+};
+
+__device__ __forceinline__ void load_mem(const KArgs& A, long long off, uint32_t slot, MemS& m) {
+    long long g = off + slot;
+    m.slot = slot;
+    m.prompt = __ldg(A.in.prompt_len + g);
+    m.tout = __ldg(A.in.true_output_len + g);
+    m.mid = __ldg(A.in.pred_len + g);
+    m.urank = __ldg(A.in.pred_urgency + g);
+    m.tie = __ldg(A.in.tie_rank + g);
+    m.dec = A.w.dec[g];
+    m.flg = A.w.flg[g];
+    m.ft = A.w.ft[g];
+}
+
+// ---- queue front / back maintenance --------------------------------------
+
+// Insert up to 32 keys (one per lane, `valid`) into the queue (FRONT+BACK).
+template <int POL>
+__device__ void q_insert32(const Env& E, Trace& T, Key key, bool valid) {
+    const KArgs& A = *E.A;
+    WarpSmem* sm = E.sm;
+    const int lane = E.lane;
+    const unsigned lt = lanemask_lt();
+    Key fmax;
+    bool have_f = T.nF > 0;
+    if (have_f) fmax = sm->F[T.nF - 1];
+    bool toF = valid && (T.nB == 0 || (have_f && klt(key, fmax)));
+    bool toB = valid && !toF;
+    unsigned bm = __ballot_sync(FULL, toB);
+    if (toB) BK(A)[T.off + T.nB + __popc(bm & lt)] = key;
+    T.nB += __popc(bm);
+    unsigned fm = __ballot_sync(FULL, toF);
+    int nI = __popc(fm);
+    if (nI == 0) return;
+    // rank of each insert among inserts
+    int ii = __popc(fm & lt);
+    if (toF) sm->X[ii] = key;
+    __syncwarp();
+    int rank_i = 0;
+    for (int k = 0; k < nI; k++) {
+        Key x = sm->X[k];
+        rank_i += klt(x, key) ? 1 : 0;
+    }
+    // position of each insert in the current FRONT (binary search)
+    int lo = 0, hi = T.nF;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (klt(sm->F[mid], key)) lo = mid + 1;
+        else hi = mid;
+    }
+    int pos_i = lo + rank_i;
+    // FRONT entries shift by the number of inserts below them
+    Key e0, e1;
+    bool h0 = lane < T.nF, h1 = lane + 32 < T.nF;
+    if (h0) e0 = sm->F[lane];
+    if (h1) e1 = sm->F[lane + 32];
+    int s0 = 0, s1 = 0;
+    for (int k = 0; k < nI; k++) {
+        Key x = sm->X[k];
+        if (h0 && klt(x, e0)) s0++;
+        if (h1 && klt(x, e1)) s1++;
+    }
+    int p0 = lane + s0, p1 = lane + 32 + s1;
+    int total = T.nF + nI;
+    __syncwarp();
+    // write back; positions >= FCAP spill to the BACK in order
+    if (h0) {
+        if (p0 < FCAP) sm->F[p0] = e0;
+        else BK(A)[T.off + T.nB + (p0 - FCAP)] = e0;
+    }
+    if (h1) {
+        if (p1 < FCAP) sm->F[p1] = e1;
+        else BK(A)[T.off + T.nB + (p1 - FCAP)] = e1;
+    }
+    if (toF) {
+        if (pos_i < FCAP) sm->F[pos_i] = key;
+        else BK(A)[T.off + T.nB + (pos_i - FCAP)] = key;
+    }
+    __syncwarp();
+    if (total > FCAP) {
+        T.nB += total - FCAP;
+        T.nF = FCAP;
+    } else {
+        T.nF = total;
+    }
+}
+
+// Remove FRONT entries flagged in `rm` (bit i = FRONT[i]).
+__device__ void f_compact(const Env& E, Trace& T, unsigned long long rm) {
+    if (rm == 0ull) return;
+    WarpSmem* sm = E.sm;
+    const int lane = E.lane;
+    const unsigned lt = lanemask_lt();
+    bool k0 = lane < T.nF && !((rm >> lane) & 1ull);
+    bool k1 = lane + 32 < T.nF && !((rm >> (lane + 32)) & 1ull);
+    unsigned b0 = __ballot_sync(FULL, k0), b1 = __ballot_sync(FULL, k1);
+    Key e0, e1;
+    if (k0) e0 = sm->F[lane];
+    if (k1) e1 = sm->F[lane + 32];
+    __syncwarp();
+    if (k0) sm->F[__popc(b0 & lt)] = e0;
+    if (k1) sm->F[__popc(b0) + __popc(b1 & lt)] = e1;
+    __syncwarp();
+    T.nF = __popc(b0) + __popc(b1);
+}
+
+// Bitonic sort of one key per lane; ascending if `asc`.
+__device__ __forceinline__ Key bitonic32(Key x, int lane, bool asc) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            Key y = kshfl_xor(x, j);
+            bool up = ((lane & k) == 0) == asc;
+            bool lower = (lane & j) == 0;
+            bool take_min = (lower == up);
+            bool ylt = klt(y, x);
+            if (take_min ? ylt : klt(x, y)) x = y;
+        }
+    }
+    return x;
+}
+
+// Move the 32 smallest BACK keys (or all of them) behind the FRONT.
+__device__ void refill(const Env& E, Trace& T) {
+    const KArgs& A = *E.A;
+    WarpSmem* sm = E.sm;
+    const int lane = E.lane;
+    Key S = kinf();  // running top-32, ascending across lanes
+    for (int base = 0; base < T.nB; base += 32) {
+        int i = base + lane;
+        Key x = i < T.nB ? BK(A)[T.off + i] : kinf();
+        Key smax = kshfl(S, 31);
+        if (!__any_sync(FULL, klt(x, smax))) continue;
+        x = bitonic32(x, lane, false);                 // descending
+        if (klt(x, S)) S = x;                          // bitonic sequence
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {             // merge ascending
+            Key y = kshfl_xor(S, j);
+            bool lower = (lane & j) == 0;
+            if (lower ? klt(y, S) : klt(S, y)) S = y;
+        }
+    }
+    int K = T.nB < 32 ? T.nB : 32;
+    if (lane < K) sm->F[T.nF + lane] = S;
+    Key thr = kshfl(S, K - 1);
+    __syncwarp();
+    T.nF += K;
+    // compact the BACK, dropping the K selected keys (all <= thr)
+    const unsigned lt = lanemask_lt();
+    int w = 0;
+    for (int base = 0; base < T.nB; base += 32) {
+        int i = base + lane;
+        Key x;
+        bool keep = false;
+        if (i < T.nB) {
+            x = BK(A)[T.off + i];
+            keep = klt(thr, x);
+        }
+        unsigned km = __ballot_sync(FULL, keep);
+        __syncwarp();
+        if (keep) BK(A)[T.off + w + __popc(km & lt)] = x;
+        w += __popc(km);
+        __syncwarp();
+    }
+    T.nB = w;
+}
+
+// ---- logging / digest -----------------------------------------------------
+__device__ __forceinline__ void log_put(Trace& T, long long pos, uint32_t v) {
+    if (T.log && pos < T.logcap) T.log[pos] = v;
+}
+
+// ---- eviction -------------------------------------------------------------
+
+struct Round {
+    unsigned G;          // granted batch positions
+    unsigned evmask;     // positions evicted with a recorded decision
+    int ndec;            // recorded decisions this round
+    unsigned long long dpend;  // digest terms of the current eviction call (lane 0)
+    unsigned long long rmF;    // FRONT entries to drop at the rebuild
+};
+
+
+// Evict one victim for member `kslot`; returns false if none is evictable.
+// `mem` is the caller lane's batch member (refreshed if it is the victim).
+template <int POL>
+__device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int m, MemS& mem,
+                          unsigned& vcall) {
+    const KArgs& A = *E.A;
+    WarpSmem* sm = E.sm;
+    const int lane = E.lane;
+    const ss_profile& P = A.P.profile;
+    // arg-max of the dispatch key over residents that are not protected
+    Key best;
+    bool have = false;
+    int best_ri = -1;
+    for (int base = 0; base < T.nR; base += 32) {
+        int i = base + lane;
+        if (i < T.nR) {
+            uint32_t s = A.w.R[T.off + i];
+            long long g = T.off + s;
+            uint32_t f = A.w.flg[g];
+            if (!(f & F_GRANT) && s != kslot) {
+                Key k = make_key<POL>(__ldg(A.in.pred_urgency + g), A.w.ft[g], __ldg(A.in.tie_rank + g), s, true);
+                if (!have || klt(best, k)) {
+                    best = k;
+                    have = true;
+                    best_ri = i;
+                }
+            }
+        }
+    }
+    if (!have) best.hi = 0, best.lo = 0, best.aux = 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        Key ok = kshfl_xor(best, o);
+        bool oh = __shfl_xor_sync(FULL, have, o);
+        int ori = __shfl_xor_sync(FULL, best_ri, o);
+        if (oh && (!have || klt(best, ok))) {
+            best = ok;
+            have = true;
+            best_ri = ori;
+        }
+    }
+    if (!have) return false;
+    const uint32_t v = best.aux & SLOT_MASK;
+    const long long gv = T.off + v;
+    // ---- should_recompute (kvcache.py:81-134), computed redundantly per lane
+    uint32_t prompt = __ldg(A.in.prompt_len + gv), mid = __ldg(A.in.pred_len + gv);
+    uint32_t dec = A.w.dec[gv], flg = A.w.flg[gv];
+    double ftb = A.w.ft[gv];
+    long long freed = (long long)prompt + dec;
+    bool pf = (flg & F_PF) != 0;
+    int action;
+    long long psaved;
+    if (pf && should_cache_prefill(prompt, P)) {
+        action = 0;
+        psaved = prompt;
+    } else {
+        action = 1;
+        psaved = 0;
+        pf = false;
+    }
+    long long saved = dec > 0 ? optimal_save_tokens(prompt, dec, P) : 0;
+    if (action == 1 && A.P.dependency_rule) saved = 0;
+    long long discarded = (long long)dec - saved;
+    long long kvh = psaved + saved;
+    double fta = remaining_time(prompt, mid, pf ? prompt : 0, saved, kvh, P);
+    T.used -= freed;
+    // where is it? batch member (by lane), pushed-back/ins, FRONT, BACK
+    unsigned bpos = __ballot_sync(FULL, lane < m && mem.slot == v);
+    uint32_t nflg = (flg & ~(F_STAGE | F_PF)) | ST_WAIT | (pf ? F_PF : 0u);
+    if ((flg & F_Q) && !(flg & F_INS)) {
+        // in FRONT or BACK: delete by slot
+        bool f0 = lane < T.nF && (sm->F[lane].aux & SLOT_MASK) == v;
+        bool f1 = lane + 32 < T.nF && (sm->F[lane + 32].aux & SLOT_MASK) == v;
+        unsigned m0 = __ballot_sync(FULL, f0), m1 = __ballot_sync(FULL, f1);
+        if (m0 | m1) {
+            if (m0) R.rmF |= 1ull << (__ffs(m0) - 1);
+            else R.rmF |= 1ull << (32 + __ffs(m1) - 1);
+        } else {
+            int found = -1;
+            for (int base = 0; base < T.nB && found < 0; base += 32) {
+                int i = base + lane;
+                bool hit = i < T.nB && (BK(A)[T.off + i].aux & SLOT_MASK) == v;
+                unsigned hm = __ballot_sync(FULL, hit);
+                if (hm) found = base + __ffs(hm) - 1;
+            }
+            if (found >= 0) {
+                if (lane == 0) BK(A)[T.off + found] = BK(A)[T.off + T.nB - 1];
+                T.nB -= 1;
+            }
+        }
+        nflg &= ~F_Q;
+    }
+    const bool add_ins = !(nflg & F_INS);
+    if (lane == 0) {
+        // release the resident slot (swap-remove)
+        uint32_t last = A.w.R[T.off + T.nR - 1];
+        A.w.R[T.off + best_ri] = last;
+        A.w.rpos[T.off + last] = (uint32_t)best_ri;
+        // state write-back
+        if (add_ins) A.w.ins[T.off + T.nins] = v;
+        nflg |= F_Q | F_INS;
+        A.w.flg[gv] = nflg;
+        A.w.dec[gv] = (uint32_t)saved;
+        A.w.ft[gv] = fta;
+        A.out.req.evictions[gv] += 1u;
+        // decision record (logged / digested only if the call succeeds)
+        int d = R.ndec;
+        if (T.log) {
+            long long p = T.logpos + SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * d;
+            unsigned long long fb = dbits(ftb), fa = dbits(fta);
+            log_put(T, p + 0, v);
+            log_put(T, p + 1, (uint32_t)action);
+            log_put(T, p + 2, (uint32_t)saved);
+            log_put(T, p + 3, (uint32_t)discarded);
+            log_put(T, p + 4, (uint32_t)freed);
+            log_put(T, p + 5, (uint32_t)fb);
+            log_put(T, p + 6, (uint32_t)(fb >> 32));
+            log_put(T, p + 7, (uint32_t)fa);
+            log_put(T, p + 8, (uint32_t)(fa >> 32));
+        }
+        if (A.P.flags & SS_FLAG_DIGEST) {
+            unsigned long long r = (unsigned long long)T.rounds;
+            R.dpend += ss_term(r, SS_TAG_EV0, d, (unsigned long long)v | ((unsigned long long)action << 32));
+            R.dpend += ss_term(r, SS_TAG_EV1, d,
+                               (unsigned long long)(uint32_t)saved | ((unsigned long long)(uint32_t)discarded << 32));
+            R.dpend += ss_term(r, SS_TAG_EV2, d, (unsigned long long)freed);
+            R.dpend += ss_term(r, SS_TAG_EV3, d, dbits(ftb));
+            R.dpend += ss_term(r, SS_TAG_EV4, d, dbits(fta));
+        }
+    }
+    if (add_ins) T.nins += 1;
+    T.nR -= 1;
+    R.ndec += 1;
+    __syncwarp();
+    if (bpos) {
+        int p = __ffs(bpos) - 1;
+        vcall |= 1u << p;
+        if (lane == p) load_mem(A, T.off, v, mem);
+    }
+    __syncwarp();
+    return true;
+}
+
+// ---- per-lane member quantities ------------------------------------------
+struct MemQ {
+    bool isdec, pf;
+    long long pfn, kvh, kvd, imm, est;
+};
+__device__ __forceinline__ MemQ mem_q(const MemS& m) {
+    MemQ q;
+    q.isdec = (m.flg & F_STAGE) == ST_DEC;
+    q.pf = (m.flg & F_PF) != 0;
+    q.pfn = q.pf ? (long long)m.prompt : 0;
+    q.kvh = q.isdec ? 0 : q.pfn + m.dec;
+    q.kvd = q.isdec ? (long long)m.prompt + m.dec : 0;
+    q.imm = q.isdec ? 1 : q.kvh + ((long long)m.prompt - q.pfn) + 1;
+    long long e = (long long)m.prompt + m.mid - q.kvd;
+    q.est = e > 0 ? e : 0;
+    return q;
+}
+
+__device__ __forceinline__ void set_status(Trace& T, int st) {
+    if (T.status == SS_TRACE_OK) T.status = st;
+}
+
+// --------------------------------------------------------------------------
+// the kernel
+// --------------------------------------------------------------------------
+template <int POL>
+__global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const KArgs& A = args;
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    WarpSmem* sm = reinterpret_cast<WarpSmem*>(smem_raw) + wib;
+    Env E{&A, sm, lane};
+    const ss_profile& P = A.P.profile;
+    const int b = A.P.batch_size;
+    const unsigned lt = lanemask_lt();
+
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(A.w.next_trace, 1);
+        t = __shfl_sync(FULL, t, 0);
+        if (t >= A.in.n_traces) break;
+
+        Trace T;
+        T.off = A.in.trace_offsets[t];
+        T.n = (int)(A.in.trace_offsets[t + 1] - T.off);
+        T.cap = A.P.memory_capacity;
+        T.clock = 0.0;
+        T.used = 0;
+        T.nF = T.nB = T.nR = T.nO = T.nins = 0;
+        T.rounds = T.evictions = T.peak = 0;
+        T.status = SS_TRACE_OK;
+        T.nuns = 0;
+        T.lost = T.anomalies = 0;
+        T.logpos = 0;
+        T.log = nullptr;
+        T.logcap = 0;
+        if ((A.P.flags & SS_FLAG_ROUND_LOG) && A.out.round_log && A.out.log_offsets) {
+            T.log = A.out.round_log + A.out.log_offsets[t];
+            T.logcap = A.out.log_offsets[t + 1] - A.out.log_offsets[t];
+        }
+        unsigned long long dig = 0ull;
+
+        // ---- init (engine.py:183-199): f_t, pre-filter, pending list
+        T.npend = 0;
+        for (int base = 0; base < T.n; base += 32) {
+            int i = base + lane;
+            bool v = i < T.n;
+            bool serv = false;
+            if (v) {
+                long long g = T.off + i;
+                uint32_t prompt = A.in.prompt_len[g], mid = A.in.pred_len[g];
+                A.w.ft[g] = remaining_time(prompt, mid, 0, 0, 0, P);
+                A.w.dec[g] = 0u;
+                A.w.flg[g] = ST_WAIT;
+                A.out.req.first_scheduled[g] = __longlong_as_double(0x7ff8000000000000ll);
+                A.out.req.finish_time[g] = __longlong_as_double(0x7ff8000000000000ll);
+                A.out.req.evictions[g] = 0u;
+                serv = (long long)prompt + 1 <= T.cap;
+                if (!serv) A.w.flg[g] = ST_UNS;
+            }
+            unsigned sm_ = __ballot_sync(FULL, v && serv), um = __ballot_sync(FULL, v && !serv);
+            if (v && serv) A.w.pend[T.off + T.npend + __popc(sm_ & lt)] = (uint32_t)i;
+            if (v && !serv) A.out.unservable_slots[T.off + T.nuns + __popc(um & lt)] = (uint32_t)i;
+            T.npend += __popc(sm_);
+            T.nuns += __popc(um);
+        }
+        T.cursor = 0;
+        __syncwarp();
+
+        MemS om;          // ongoing member held by this lane (lane < nO)
+        Key okey;         // its dispatch key
+        om.slot = 0;
+
+        // ---- the round loop (engine.py:202-224)
+        while (T.status == SS_TRACE_OK) {
+            // admission of prediction-ready requests (engine.py:204-206)
+            {
+                double thr = ss::add(T.clock, 1e-12);
+                while (T.cursor < T.npend) {
+                    int i = T.cursor + lane;
+                    bool v = i < T.npend;
+                    uint32_t s = 0;
+                    bool ok = false;
+                    if (v) {
+                        s = A.w.pend[T.off + i];
+                        ok = A.in.ready_time[T.off + s] <= thr;
+                    }
+                    unsigned am = __ballot_sync(FULL, ok);
+                    int cnt = __ffs(~am) - 1;
+                    if (am == FULL) cnt = 32;
+                    if (cnt == 0) break;
+                    bool mine = lane < cnt;
+                    Key k;
+                    if (mine) {
+                        long long g = T.off + s;
+                        A.w.flg[g] = ST_WAIT | F_Q;
+                        k = make_key<POL>(__ldg(A.in.pred_urgency + g), A.w.ft[g], __ldg(A.in.tie_rank + g), s, false);
+                    }
+                    q_insert32<POL>(E, T, k, mine);
+                    T.cursor += cnt;
+                    if (cnt < 32) break;
+                }
+            }
+            int live = T.nF + T.nB + T.nO;
+            if (live == 0) {
+                if (T.cursor >= T.npend) break;
+                T.clock = A.in.ready_time[T.off + A.w.pend[T.off + T.cursor]];
+                continue;
+            }
+            if (T.nF < b && T.nB > 0) refill(E, T);
+
+            // ---- stage-aware composition (batching.py:46-88)
+            const int nc = T.nF < b ? T.nF : b;
+            const bool has_c = lane < nc;
+            const bool has_o = lane < T.nO;
+            Key ck;
+            MemS cm;
+            if (has_c) {
+                ck = sm->F[lane];
+                load_mem(A, T.off, ck.aux & SLOT_MASK, cm);  // prefetch, used if selected
+            }
+            // p* = min(C[0], min ongoing)
+            Key omin = has_o ? okey : kinf();
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                Key x = kshfl_xor(omin, o);
+                if (klt(x, omin)) omin = x;
+            }
+            bool pstar_prefill;
+            if (nc > 0 && (T.nO == 0 || klt(sm->F[0], omin))) pstar_prefill = !(sm->F[0].aux & DEC_BIT);
+            else pstar_prefill = false;
+            const int kind = pstar_prefill ? SS_KIND_PREFILL : SS_KIND_DECODE;
+            const bool c_elig = has_c && (pstar_prefill || (ck.aux & DEC_BIT));
+            const unsigned cmask = __ballot_sync(FULL, c_elig);
+            if (has_o) sm->X[lane] = okey;
+            __syncwarp();
+            int cnt_c = 0, cnt_o = 0;
+            for (int k = 0; k < T.nO; k++) {
+                Key x = sm->X[k];
+                if (c_elig && klt(x, ck)) cnt_c++;
+                if (has_o && klt(x, okey)) cnt_o++;
+            }
+            if (has_o) {
+                int lo = 0, hi = nc;
+                while (lo < hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (klt(sm->F[mid], okey)) lo = mid + 1;
+                    else hi = mid;
+                }
+                unsigned below = lo >= 32 ? FULL : ((1u << lo) - 1u);
+                cnt_o += __popc(cmask & below);
+            }
+            const int c_rank = __popc(cmask & lt) + cnt_c;
+            const int elig = __popc(cmask) + T.nO;
+            const int m = elig < b ? elig : b;
+            __syncwarp();
+            if (c_elig && c_rank < m) {
+                // popped from the heap for good: no longer queued
+                cm.flg &= ~F_Q;
+                A.w.flg[T.off + cm.slot] = cm.flg;
+                sm->M[c_rank] = cm;
+            }
+            if (has_o && cnt_o < m) sm->M[cnt_o] = om;
+            bool pushed_o = has_o && cnt_o >= m;   // merged[b:] from ongoing -> heap
+            __syncwarp();
+            MemS mem;
+            mem.slot = 0;
+            if (lane < m) mem = sm->M[lane];
+            Round R;
+            R.G = 0;
+            R.evmask = 0;
+            R.ndec = 0;
+            R.dpend = 0ull;
+            R.rmF = (unsigned long long)__ballot_sync(FULL, c_elig && c_rank < m);
+            // pushed-back ongoing members go back to the queue
+            {
+                unsigned pm = __ballot_sync(FULL, pushed_o);
+                if (pushed_o) {
+                    long long g = T.off + om.slot;
+                    A.w.flg[g] = om.flg | F_Q | F_INS;
+                    A.w.ins[T.off + T.nins + __popc(pm & lt)] = om.slot;
+                }
+                T.nins += __popc(pm);
+            }
+            const int nO_start = T.nO;
+            const int nuns_start = T.nuns;
+            __syncwarp();
+
+            // ---- admission with KV budget (engine.py:296-327)
+            const bool act = lane < m;
+            MemQ q = mem_q(mem);
+            {
+                long long inc = act ? q.imm : 0;
+                long long excl = warp_incl_scan_ll(inc, lane) - inc;
+                long long dem = q.est > q.imm ? q.est : q.imm;
+                if (dem + excl > T.cap) dem = q.imm;
+                bool need = act && (dem + excl + T.used > T.cap);
+                unsigned nm = __ballot_sync(FULL, need);
+                const unsigned mmask = m >= 32 ? FULL : ((1u << m) - 1u);
+                if (nm == 0) {
+                    R.G = mmask;
+                } else {
+                    // slow path: one member at a time from the first that must evict
+                    int f = __ffs(nm) - 1;
+                    R.G = (1u << f) - 1u;
+                    long long reserved = __shfl_sync(FULL, excl, f);
+                    if (act && lane < f) {
+                        mem.flg |= F_GRANT;
+                        A.w.flg[T.off + mem.slot] = mem.flg;
+                    }
+                    __syncwarp();
+                    for (int k = f; k < m && T.status == SS_TRACE_OK; k++) {
+                        if ((R.evmask >> k) & 1u) continue;
+                        q = mem_q(mem);
+                        long long imm_k = __shfl_sync(FULL, q.imm, k);
+                        long long est_k = __shfl_sync(FULL, q.est, k);
+                        long long kvd_k = __shfl_sync(FULL, q.kvd, k);
+                        uint32_t slot_k = __shfl_sync(FULL, mem.slot, k);
+                        uint32_t flg_k = __shfl_sync(FULL, mem.flg, k);
+                        const bool isdec_k = __shfl_sync(FULL, (int)q.isdec, k) != 0;
+                        long long dem_k = est_k > imm_k ? est_k : imm_k;
+                        if (dem_k + reserved > T.cap) dem_k = imm_k;
+                        long long demand = dem_k + reserved;
+                        int d0 = R.ndec;
+                        unsigned vcall = 0;
+                        R.dpend = 0ull;
+                        bool ok = true;
+                        while (demand + T.used > T.cap) {
+                            if (!evict_one<POL>(E, T, R, slot_k, m, mem, vcall)) {
+                                ok = false;
+                                break;
+                            }
+                        }
+                        if (!ok) {
+                            // AdmissionFailure: evictions stand, decisions are lost
+                            T.lost += R.ndec - d0;
+                            R.ndec = d0;
+                            // re-read member k (it may not have changed)
+                            flg_k = __shfl_sync(FULL, mem.flg, k);
+                            if (kvd_k + imm_k > T.cap) {
+                                // _mark_unservable (engine.py:402-412)
+                                if (lane == k) {
+                                    long long g = T.off + mem.slot;
+                                    if (q.isdec) {
+                                        uint32_t ri = A.w.rpos[g];
+                                        uint32_t last = A.w.R[T.off + T.nR - 1];
+                                        A.w.R[T.off + ri] = last;
+                                        A.w.rpos[T.off + last] = ri;
+                                    }
+                                    mem.flg = (mem.flg & ~(F_STAGE | F_Q | F_INS | F_GRANT)) | ST_UNS;
+                                    A.w.flg[g] = mem.flg;
+                                    A.out.unservable_slots[T.off + T.nuns] = mem.slot;
+                                }
+                                if (isdec_k) T.nR -= 1;
+                                T.used -= kvd_k;
+                                T.nuns += 1;
+                            } else if (!(flg_k & F_Q)) {
+                                if (lane == k) {
+                                    mem.flg |= F_Q | F_INS;
+                                    A.w.flg[T.off + mem.slot] = mem.flg;
+                                    A.w.ins[T.off + T.nins] = mem.slot;
+                                }
+                                T.nins += 1;
+                            }
+                            __syncwarp();
+                            continue;
+                        }
+                        // success: commit this call's decisions
+                        R.evmask |= vcall;
+                        if (lane == 0) dig += R.dpend;
+                        if (flg_k & F_Q) {
+                            // granted while still queued: the reference keeps a stale
+                            // heap entry for it -- not emulated
+                            T.anomalies += 1;
+                            set_status(T, SS_TRACE_ANOMALY);
+                        }
+                        R.G |= 1u << k;
+                        reserved += imm_k;
+                        if (lane == k) {
+                            mem.flg |= F_GRANT;
+                            A.w.flg[T.off + mem.slot] = mem.flg;
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+            if (T.status != SS_TRACE_OK) break;
+            T.evictions += R.ndec;
+            const bool g_act = (R.G >> lane) & 1u;
+            const int ng = __popc(R.G);
+            unsigned long long r64 = (unsigned long long)T.rounds;
+
+            if (ng == 0) {
+                // nothing granted (engine.py:329-344): clock does not advance
+                T.nO = 0;
+                if (A.P.flags & SS_FLAG_DIGEST) {
+                    if (lane == 0) {
+                        dig += ss_term(r64, SS_TAG_HDR, 0, ss_hdr_word(SS_KIND_NONE, 0, 0, R.ndec));
+                        dig += ss_term(r64, SS_TAG_MEM, 0, (unsigned long long)T.used);
+                        dig += ss_term(r64, SS_TAG_TIME, 0, dbits(T.clock));
+                    }
+                }
+                if (R.ndec > 0) {
+                    if (T.used > T.peak) T.peak = T.used;
+                    if (T.log) {
+                        if (lane == 0) {
+                            unsigned long long mu = (unsigned long long)T.used, tb = dbits(T.clock);
+                            log_put(T, T.logpos + 0, SS_KIND_NONE);
+                            log_put(T, T.logpos + 1, 0);
+                            log_put(T, T.logpos + 2, 0);
+                            log_put(T, T.logpos + 3, (uint32_t)R.ndec);
+                            log_put(T, T.logpos + 4, (uint32_t)mu);
+                            log_put(T, T.logpos + 5, (uint32_t)(mu >> 32));
+                            log_put(T, T.logpos + 6, (uint32_t)tb);
+                            log_put(T, T.logpos + 7, (uint32_t)(tb >> 32));
+                        }
+                        T.logpos += SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * R.ndec;
+                    }
+                }
+                T.rounds += 1;
+                if (R.ndec == 0 && T.nuns == nuns_start && nO_start == 0) set_status(T, SS_TRACE_LIVELOCK);
+            } else {
+                // ---- batch_duration (engine.py:126-149) over granted members
+                q = mem_q(mem);
+                double total = 0.0;
+                unsigned pre = __ballot_sync(FULL, g_act && !q.isdec);
+                if (pre) {
+                    double rl = reload_time(q.kvh, P);
+                    double pft = prefill_time((long long)mem.prompt - q.pfn, P);
+                    for (int k = 0; k < m; k++) {
+                        double a = __shfl_sync(FULL, rl, k), c2 = __shfl_sync(FULL, pft, k);
+                        if ((pre >> k) & 1u) {
+                            total = ss::add(total, a);
+                            total = ss::add(total, c2);
+                        }
+                    }
+                }
+                unsigned dm = __ballot_sync(FULL, g_act && q.isdec);
+                if (dm) {
+                    double st = (g_act && q.isdec)
+                                    ? decode_step_time((long long)mem.prompt + mem.dec + 1, 1, P)
+                                    : -INFINITY;
+                    double part;
+                    if (!A.P.decode_cost_sum) {
+                        part = st;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) part = fmax(part, __shfl_xor_sync(FULL, part, o));
+                    } else {
+                        PySum ps;
+                        ps.init();
+                        for (int k = 0; k < m; k++) {
+                            double x = __shfl_sync(FULL, st, k);
+                            if ((dm >> k) & 1u) ps.push(x);
+                        }
+                        part = ps.value();
+                    }
+                    total = ss::add(total, part);
+                }
+                const double end = ss::add(T.clock, total);
+
+                // ---- per-member progress (engine.py:351-363, 382-421)
+                long long delta = 0;
+                bool done = false, newres = false;
+                if (g_act) {
+                    long long g = T.off + mem.slot;
+                    if (!(mem.flg & F_FIRST)) {
+                        A.out.req.first_scheduled[g] = T.clock;
+                        mem.flg |= F_FIRST;
+                    }
+                    if (q.isdec) {
+                        delta = 1;
+                        mem.dec += 1;
+                    } else {
+                        delta = q.kvh + ((long long)mem.prompt - q.pfn);
+                        mem.flg = (mem.flg & ~F_STAGE) | ST_DEC | F_PF;
+                        newres = true;
+                    }
+                    mem.flg &= ~F_GRANT;
+                    if (mem.dec >= mem.tout) {
+                        done = true;
+                        delta -= (long long)mem.prompt + mem.dec;
+                        A.out.req.finish_time[g] = end;
+                        mem.ft = 0.0;
+                        mem.flg = (mem.flg & ~F_STAGE) | ST_DONE;
+                    } else {
+                        mem.ft = remaining_time(mem.prompt, mem.mid, mem.prompt, mem.dec, 0, P);
+                    }
+                    A.w.dec[g] = mem.dec;
+                    A.w.ft[g] = mem.ft;
+                    A.w.flg[g] = mem.flg;
+                }
+                T.used += warp_sum_ll(delta);
+                if (T.used > T.cap || T.used < 0) set_status(T, SS_TRACE_INTERNAL);
+                // resident list: newly prefilled join, completed leave
+                {
+                    unsigned nm = __ballot_sync(FULL, newres);
+                    if (newres) {
+                        uint32_t idx = (uint32_t)(T.nR + __popc(nm & lt));
+                        A.w.R[T.off + idx] = mem.slot;
+                        A.w.rpos[T.off + mem.slot] = idx;
+                    }
+                    T.nR += __popc(nm);
+                    unsigned cmk = __ballot_sync(FULL, done);
+                    __syncwarp();
+                    while (cmk) {
+                        int k = __ffs(cmk) - 1;
+                        cmk &= cmk - 1;
+                        uint32_t s = __shfl_sync(FULL, mem.slot, k);
+                        if (lane == 0) {
+                            uint32_t ri = A.w.rpos[T.off + s];
+                            uint32_t last = A.w.R[T.off + T.nR - 1];
+                            A.w.R[T.off + ri] = last;
+                            A.w.rpos[T.off + last] = ri;
+                        }
+                        T.nR -= 1;
+                        __syncwarp();
+                    }
+                }
+                // ---- ITERATION_END record (engine.py:365-380) + digest
+                const unsigned cdone = __ballot_sync(FULL, done);
+                const int nc_done = __popc(cdone);
+                const int gi = __popc(R.G & lt), ci = __popc(cdone & lt);
+                if (A.P.flags & SS_FLAG_DIGEST) {
+                    if (g_act) dig += ss_term(r64, SS_TAG_GRANT, gi, mem.slot);
+                    if (done) dig += ss_term(r64, SS_TAG_DONE, ci, mem.slot);
+                    if (lane == 0) {
+                        dig += ss_term(r64, SS_TAG_HDR, 0, ss_hdr_word(kind, ng, nc_done, R.ndec));
+                        dig += ss_term(r64, SS_TAG_MEM, 0, (unsigned long long)T.used);
+                        dig += ss_term(r64, SS_TAG_TIME, 0, dbits(end));
+                    }
+                }
+                if (T.log) {
+                    long long base = T.logpos + SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * R.ndec;
+                    if (g_act) log_put(T, base + gi, mem.slot);
+                    if (done) log_put(T, base + ng + ci, mem.slot);
+                    if (lane == 0) {
+                        unsigned long long mu = (unsigned long long)T.used, tb = dbits(end);
+                        log_put(T, T.logpos + 0, (uint32_t)kind);
+                        log_put(T, T.logpos + 1, (uint32_t)ng);
+                        log_put(T, T.logpos + 2, (uint32_t)nc_done);
+                        log_put(T, T.logpos + 3, (uint32_t)R.ndec);
+                        log_put(T, T.logpos + 4, (uint32_t)mu);
+                        log_put(T, T.logpos + 5, (uint32_t)(mu >> 32));
+                        log_put(T, T.logpos + 6, (uint32_t)tb);
+                        log_put(T, T.logpos + 7, (uint32_t)(tb >> 32));
+                    }
+                    T.logpos = base + ng + nc_done;
+                }
+                if (T.used > T.peak) T.peak = T.used;
+                T.clock = end;
+                T.rounds += 1;
+                // ---- ongoing = granted and not completed, in granted order
+                const bool stay = g_act && !done;
+                const unsigned smk = __ballot_sync(FULL, stay);
+                __syncwarp();
+                if (stay) sm->M[__popc(smk & lt)] = mem;
+                __syncwarp();
+                T.nO = __popc(smk);
+                if (lane < T.nO) {
+                    om = sm->M[lane];
+                    okey = make_key<POL>(om.urank, om.ft, om.tie, om.slot, true);
+                }
+            }
+            if (T.log && T.logpos > T.logcap) set_status(T, SS_TRACE_LOG_OVERFLOW);
+            if (A.P.max_rounds > 0 && T.rounds >= A.P.max_rounds) set_status(T, SS_TRACE_ROUND_CAP);
+
+            // ---- queue rebuild: drop taken FRONT entries, insert pushed-back,
+            //      failed and evicted requests with their current keys
+            f_compact(E, T, R.rmF);
+            for (int base = 0; base < T.nins; base += 32) {
+                int i = base + lane;
+                bool v = false;
+                Key k;
+                if (i < T.nins) {
+                    uint32_t s = A.w.ins[T.off + i];
+                    long long g = T.off + s;
+                    uint32_t f = A.w.flg[g];
+                    if (f & F_INS) {
+                        v = true;
+                        A.w.flg[g] = f & ~F_INS;
+                        k = make_key<POL>(__ldg(A.in.pred_urgency + g), A.w.ft[g], __ldg(A.in.tie_rank + g), s,
+                                          (f & F_STAGE) == ST_DEC);
+                    }
+                }
+                q_insert32<POL>(E, T, k, v);
+            }
+            T.nins = 0;
+            __syncwarp();
+        }
+
+        // ---- outputs and the fused statistics (metrics.py:35-56)
+        {
+            PySum acc;
+            acc.init();
+            int mylv = lane;  // lanes 0..15: per-level normalized wait
+            for (int base = 0; base < T.n; base += 32) {
+                int i = base + lane;
+                bool v = i < T.n;
+                double w = 0.0, nw = 0.0;
+                bool fin = false;
+                int lv = 0;
+                if (v) {
+                    long long g = T.off + i;
+                    uint32_t f = A.w.flg[g], dcount = A.w.dec[g];
+                    A.out.req.generated[g] = dcount;
+                    if (A.out.req.f_t) A.out.req.f_t[g] = A.w.ft[g];
+                    if (A.out.req.state) {
+                        uint32_t st = f & F_STAGE;
+                        A.out.req.state[g] = st | ((f & F_PF) ? 256u : 0u);
+                    }
+                    double fi = A.out.req.finish_time[g];
+                    if (!isnan(fi)) {
+                        fin = true;
+                        w = ss::sub(fi, A.in.arrival_time[g]);
+                        nw = ss::dv(w, (double)dcount);
+                        lv = A.in.true_urgency[g];
+                    }
+                }
+                unsigned fm = __ballot_sync(FULL, fin);
+                while (fm) {
+                    int k = __ffs(fm) - 1;
+                    fm &= fm - 1;
+                    double wk = __shfl_sync(FULL, w, k), nk = __shfl_sync(FULL, nw, k);
+                    int lk = __shfl_sync(FULL, lv, k);
+                    if (lane == 31) acc.push(wk);
+                    else if (lane == 30) acc.push(nk);
+                    else if (lane == lk && lane < SS_MAX_LEVELS) acc.push(nk);
+                }
+            }
+            dig = warp_sum_u64(dig);
+            double val = acc.value();
+            int cntv = acc.n;
+            __syncwarp();
+            ss_trace_stats* st = A.out.stats + t;
+            if (lane < SS_MAX_LEVELS) {
+                st->level_norm_sum[lane] = val;
+                st->level_count[lane] = cntv;
+            }
+            if (lane == 30) st->sum_norm_wait = val;
+            if (lane == 31) {
+                st->sum_wait = val;
+                st->completed = cntv;
+            }
+            if (lane == 0) {
+                st->digest = (A.P.flags & SS_FLAG_DIGEST) ? dig : 0ull;
+                st->rounds = T.rounds;
+                st->evictions = T.evictions;
+                st->mem_used_peak = T.peak;
+                st->log_words = T.log ? (T.logpos < T.logcap ? T.logpos : T.logcap) : 0;
+                st->unservable = T.nuns;
+                st->status = T.status;
+                st->lost_evictions = T.lost;
+                st->anomalies = T.anomalies;
+                st->_pad = 0;
+                st->final_clock = T.clock;
+            }
+            (void)mylv;
+        }
+        __syncwarp();
+    }
+}
+
+// --------------------------------------------------------------------------
+// host-side launch helpers
+// --------------------------------------------------------------------------
+static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+size_t work_bytes(int64_t n) {
+    size_t nn = (size_t)(n > 0 ? n : 1);
+    return align16(nn * 8) + 4 * align16(nn * 4) + align16(nn * 16) + 3 * align16(nn * 4) + 16;
+}
+
+void carve_work(void* base, int64_t n, Work* w) {
+    size_t nn = (size_t)(n > 0 ? n : 1);
+    char* p = (char*)base;
+    w->ft = (double*)p;      p += align16(nn * 8);
+    w->dec = (uint32_t*)p;   p += align16(nn * 4);
+    w->flg = (uint32_t*)p;   p += align16(nn * 4);
+    w->rpos = (uint32_t*)p;  p += align16(nn * 4);
+    w->R = (uint32_t*)p;     p += align16(nn * 4);
+    w->B = (void*)p;         p += align16(nn * 16);
+    w->pend = (uint32_t*)p;  p += align16(nn * 4);
+    w->ins = (uint32_t*)p;   p += align16(nn * 4);
+    p += align16(nn * 4);
+    w->next_trace = (int*)p;
+}
+
+int sched_smem_bytes() { return (int)(sizeof(WarpSmem) * WPB); }
+
+template <int POL>
+static const void* kernel_ptr() { return (const void*)sched_kernel<POL>; }
+
+static const void* kernel_for(int policy) {
+    switch (policy) {
+    case SS_POLICY_SEMANTIC: return kernel_ptr<SS_POLICY_SEMANTIC>();
+    default: return nullptr;
+    }
+}
+
+int sched_max_blocks(int policy, int* sm_count) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const void* k = kernel_for(policy);
+    if (!k) return 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 32 * WPB, sched_smem_bytes());
+    if (sm_count) *sm_count = sms;
+    return per * sms;
+}
+
+int launch_sched(const KArgs& a, int blocks, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    size_t smem = (size_t)sched_smem_bytes();
+    switch (a.P.policy) {
+    case SS_POLICY_SEMANTIC:
+        sched_kernel<SS_POLICY_SEMANTIC><<<blocks, 32 * WPB, smem, st>>>(a);
+        break;
+    default:
+        return SS_ERR_UNSUPPORTED;
+    }
+    return cudaGetLastError() == cudaSuccess ? SS_OK : SS_ERR_CUDA;
+}
+
+}  // namespace ss

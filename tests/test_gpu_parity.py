@@ -1,0 +1,153 @@
+"""CUDA scheduler vs the reference (golden fixtures) and vs the oracle.
+
+Bit-exact: schedules (per-round logs), eviction decisions, unservable lists,
+per-request first_scheduled / finish_time (float64 bit patterns),
+generated tokens, eviction counts, final f_t, round counts and digests."""
+
+import numpy as np
+import pytest
+
+from conftest import case_batch, case_params, golden_cases
+from parity_helpers import check_against_golden
+from paper_2506_12204_b200 import _abi as A
+
+pytestmark = pytest.mark.gpu
+
+SMALL = [c for c in golden_cases("small") if c["params"]["policy"] == "semantic"]
+LARGE = [c for c in golden_cases("large") if c["params"]["policy"] == "semantic"]
+
+
+@pytest.fixture(scope="module")
+def native():
+    from paper_2506_12204_b200 import native as nat
+
+    nat.device_info()  # raises if no GPU / no extension
+    return nat
+
+
+@pytest.mark.parametrize("case", SMALL, ids=[c["name"] for c in SMALL])
+def test_gpu_matches_reference_small(native, case):
+    batch = case_batch(case)
+    res = native.run_host(case_params(case, A.SS_FLAG_DIGEST), batch, want_log=True)
+    check_against_golden(res, case, batch=batch)
+
+
+@pytest.mark.parametrize("case", LARGE, ids=[c["name"] for c in LARGE])
+def test_gpu_matches_reference_large(native, case):
+    batch = case_batch(case)
+    res = native.run_host(case_params(case, A.SS_FLAG_DIGEST), batch, want_log=False)
+    check_against_golden(res, case, batch=batch)
+
+
+def _seeded_batch(n_traces, total, cfg_kw=None, seed0=0):
+    from paper_2506_12204_b200.engine import ScenarioConfig
+    from paper_2506_12204_b200.soa import TraceBatch, prepare_trace
+    from paper_2506_12204_b200.workload import WorkloadSpec, generate
+
+    parts = []
+    cfg = None
+    for s in range(seed0, seed0 + n_traces):
+        cfg = ScenarioConfig(workload=WorkloadSpec(total_requests=total, seed=s, **(cfg_kw or {})), seed=s)
+        parts.append(prepare_trace(generate(cfg.workload), cfg)[0])
+    return TraceBatch.concat(parts), cfg
+
+
+def _compare_with_oracle(gpu, cpu):
+    from paper_2506_12204_b200 import _abi as A
+
+    for k in ("status", "rounds", "evictions", "digest", "completed", "unservable", "mem_used_peak",
+              "lost_evictions"):
+        assert np.array_equal(gpu.stats[k], cpu.stats[k]), k
+    assert np.array_equal(gpu.stats["final_clock"].view(np.uint64), cpu.stats["final_clock"].view(np.uint64))
+    for k in ("first_scheduled", "finish_time", "f_t"):
+        assert np.array_equal(getattr(gpu, k).view(np.uint64), getattr(cpu, k).view(np.uint64)), k
+    for k in ("generated", "evictions"):
+        assert np.array_equal(getattr(gpu, k), getattr(cpu, k)), k
+    # fused statistics: bit-exact CPython-3.12 sums
+    for k in ("sum_wait", "sum_norm_wait", "level_norm_sum"):
+        assert np.array_equal(gpu.stats[k].view(np.uint64), cpu.stats[k].view(np.uint64)), k
+    assert np.array_equal(gpu.stats["level_count"], cpu.stats["level_count"])
+
+
+@pytest.mark.parametrize("capacity", [10**9, 1500, 700])
+def test_gpu_many_traces_vs_oracle(native, capacity):
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.results import make_params
+
+    batch, cfg = _seeded_batch(96, 300, dict(levels=3))
+    p = lambda: make_params(cfg.gpu_profile(), 16, capacity, levels=3, flags=A.SS_FLAG_DIGEST)
+    gpu = native.run_host(p(), batch)
+    cpu = run_oracle(p(), batch, threads=8)
+    assert (cpu.stats["status"] == 0).all()
+    _compare_with_oracle(gpu, cpu)
+
+
+@pytest.mark.parametrize("prof", ["a100_qwen7b", "a5000_qwen7b", "mixed"])
+@pytest.mark.parametrize("b", [1, 7, 16, 32])
+def test_gpu_batch_sizes_profiles_vs_oracle(native, prof, b):
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.results import make_params
+    from paper_2506_12204_b200.scenarios import MIXED_PROFILE
+
+    pr = MIXED_PROFILE if prof == "mixed" else get_profile(prof)
+    batch, _ = _seeded_batch(24, 200, dict(levels=4, output_len_range=(1, 300)), seed0=100 + b)
+    for dep, cost in ((True, "max"), (False, "sum")):
+        p = lambda: make_params(pr, b, 800, levels=4, dependency_rule=dep, decode_batch_cost=cost,
+                                flags=A.SS_FLAG_DIGEST)
+        gpu = native.run_host(p(), batch)
+        cpu = run_oracle(p(), batch, threads=8)
+        ok = cpu.stats["status"] == 0
+        assert np.array_equal(gpu.stats["status"][ok], cpu.stats["status"][ok])
+        if ok.all():
+            _compare_with_oracle(gpu, cpu)
+
+
+def test_gpu_round_logs_vs_oracle(native):
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.results import make_params
+
+    batch, cfg = _seeded_batch(8, 150, dict(levels=3))
+    gpu = native.run_host(make_params(cfg.gpu_profile(), 8, 600, levels=3), batch, want_log=True)
+    cpu = run_oracle(make_params(cfg.gpu_profile(), 8, 600, levels=3, flags=A.SS_FLAG_DIGEST | A.SS_FLAG_ROUND_LOG),
+                     batch)
+    for t in range(batch.n_traces):
+        if cpu.stats["status"][t] == 0:
+            assert np.array_equal(gpu.logs[t], cpu.logs[t]), t
+
+
+def test_run_dropin_matches_golden(native):
+    """engine.run() rebuilds the reference Trace (records, events, unservable)."""
+    from paper_2506_12204_b200 import Request, UrgencyLevel
+    from paper_2506_12204_b200.engine import EventKind, Policy, ScenarioConfig, run
+    from paper_2506_12204_b200.costs import GpuProfile
+    from paper_2506_12204_b200.predictors import PredictorConfig, Strategy
+    from paper_2506_12204_b200.workload import WorkloadSpec
+
+    for case in SMALL:
+        p = case["params"]
+        prof = GpuProfile("x", **p["profile"])
+        wl = WorkloadSpec(**{**p["workload"], "prompt_len_range": tuple(p["workload"]["prompt_len_range"]),
+                             "output_len_range": tuple(p["workload"]["output_len_range"])})
+        pc = p["predictor"]
+        cfg = ScenarioConfig(policy=Policy(p["policy"]), profile_override=prof, batch_size=p["batch_size"],
+                             memory_capacity=p["memory_capacity"], workload=wl,
+                             predictor=PredictorConfig(latency_s=pc["latency_s"], batch_size=pc["batch_size"],
+                                                       strategy=Strategy(pc["strategy"]),
+                                                       urgency_error=pc["urgency_error"],
+                                                       length_error=pc["length_error"]),
+                             seed=p["seed"], dependency_rule=p["dependency_rule"],
+                             decode_batch_cost=p["decode_batch_cost"])
+        arrivals = [Request(id=i, arrival_time=a, prompt_len=pl, true_output_len=o,
+                            true_urgency=UrgencyLevel(u, wl.levels)) for i, a, pl, o, u in case["arrivals"]]
+        tr = run(cfg, arrivals)
+        exp = case["expected"]
+        assert len(tr.events) == exp["n_events"], case["name"]
+        assert tr.unservable == exp["unservable"]
+        assert tr.eviction_count == exp["eviction_count"]
+        for rec, want in zip(tr.records, exp["records"]):
+            assert rec.id == want[0]
+            assert rec.first_scheduled == want[1] and rec.finish_time == want[2], case["name"]
+            assert rec.generated_tokens == want[3] and rec.evictions == want[4]
+        ends = [e for e in tr.events if e.kind is EventKind.ITERATION_END]
+        assert len(ends) == len(exp["log"])
