@@ -55,9 +55,11 @@ extern "C" {
 #define SS_TRACE_ROUND_CAP    2  /* params.max_rounds reached                    */
 #define SS_TRACE_LOG_OVERFLOW 3  /* round log region too small                   */
 #define SS_TRACE_INTERNAL     4  /* invariant violated (allocation > free, ...)  */
-#define SS_TRACE_ANOMALY      5  /* a request was granted while still queued: the
-                                    reference keeps a stale heap entry for it
-                                    (DESIGN.md §5); not emulated                 */
+#define SS_TRACE_REF_ERROR    6  /* the reference raises an exception on this
+                                    trace (IllegalTransitionError,
+                                    DuplicateRequestError, ValueError from
+                                    estimate_kv_size on a completed request or an
+                                    uncaught AdmissionFailure)  */
 
 /* ---- policies (engine.py:40-44, keys engine.py:114-123) ---------------- */
 #define SS_POLICY_SEMANTIC 0
@@ -124,7 +126,9 @@ typedef struct ss_trace_stats {
     int32_t  status;           /* SS_TRACE_*                                       */
     int32_t  lost_evictions;   /* evictions made by an admission that then failed:
                                   applied but, as in the reference, not recorded   */
-    int32_t  anomalies;        /* granted while still queued    */
+    int32_t  anomalies;        /* grants of a request that still had a heap entry
+                                  (the reference then carries a stale key and
+                                  duplicate batch members; emulated) */
     int32_t  _pad;
     double   final_clock;      /* RUN_END time                                     */
     /* CPython-3.12 float sum() (Neumaier) over completed records in trace order  */

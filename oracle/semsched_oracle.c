@@ -268,7 +268,7 @@ static okey key_of(const osim* s, int i) {                 /* engine.py:114-123 
     return k;
 }
 static void heap_insert(osim* s, int i) {
-    if (h_contains(&s->heap, i)) { s->status = SS_TRACE_INTERNAL; return; } /* DuplicateRequestError */
+    if (h_contains(&s->heap, i)) { s->status = SS_TRACE_REF_ERROR; return; } /* DuplicateRequestError */
     h_insert(&s->heap, i, key_of(s, i));
 }
 static void evq_insert(osim* s, int i) { h_insert(&s->evq, i, key_neg(key_of(s, i))); }
@@ -512,6 +512,10 @@ static void execute(osim* s, int kind, int m) {
         int i = batch[k];
         oreq* r = &s->r[i];
         if (s->evicted_flag[i]) continue;                          /* :297-298 */
+        if (r->stage == ST_COMPLETED) {                            /* estimate_kv_size: ValueError */
+            s->status = SS_TRACE_REF_ERROR;
+            return;
+        }
         int64_t immediate = r->stage == ST_DECODING ? 1 : r->kv_host + (r->prompt - r->prefilled) + 1;
         int64_t est = estimate_kv_size(r);
         int64_t demand = est > immediate ? est : immediate;
@@ -569,23 +573,27 @@ static void execute(osim* s, int kind, int m) {
         int i = s->granted[k];
         oreq* r = &s->r[i];
         if (isnan(r->first_sched)) r->first_sched = s->clock;
+        if (r->stage == ST_COMPLETED) {                            /* transition(PREFILLING) */
+            s->status = SS_TRACE_REF_ERROR;
+            return;
+        }
         if (r->stage == ST_DECODING) {                             /* _decode_step */
-            if (1 > s->cap - s->used) s->status = SS_TRACE_INTERNAL;
+            if (1 > s->cap - s->used) s->status = SS_TRACE_REF_ERROR;
             s->used += 1; r->kv_dev += 1; r->decoded += 1;
         } else {                                                   /* _prefill_round */
             if (r->kv_host > 0) {
-                if (r->kv_host > s->cap - s->used) s->status = SS_TRACE_INTERNAL;
+                if (r->kv_host > s->cap - s->used) s->status = SS_TRACE_REF_ERROR;
                 s->used += r->kv_host; r->kv_dev += r->kv_host; r->kv_host = 0;
             }
             int64_t to_prefill = r->prompt - r->prefilled;
             if (to_prefill > 0) {
-                if (to_prefill > s->cap - s->used) s->status = SS_TRACE_INTERNAL;
+                if (to_prefill > s->cap - s->used) s->status = SS_TRACE_REF_ERROR;
                 s->used += to_prefill; r->kv_dev += to_prefill; r->prefilled = r->prompt;
             }
             r->stage = ST_DECODING;                                /* PREFILLING -> DECODING */
         }
         if (r->decoded >= r->true_out) {                           /* _complete */
-            if (r->stage == ST_COMPLETED) { s->status = SS_TRACE_INTERNAL; continue; } /* IllegalTransition */
+            if (r->stage == ST_COMPLETED) { s->status = SS_TRACE_REF_ERROR; return; } /* IllegalTransition */
             if (h_contains(&s->evq, i)) h_remove_at(&s->evq, r->gpos);
             s->used -= r->kv_dev; r->kv_dev = 0;
             r->finish = end; r->f_t = 0.0; r->stage = ST_COMPLETED;

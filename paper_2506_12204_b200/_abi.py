@@ -20,9 +20,9 @@ SS_TRACE_LIVELOCK = 1
 SS_TRACE_ROUND_CAP = 2
 SS_TRACE_LOG_OVERFLOW = 3
 SS_TRACE_INTERNAL = 4
-SS_TRACE_ANOMALY = 5
+SS_TRACE_REF_ERROR = 6
 TRACE_STATUS_NAMES = {0: "ok", 1: "livelock", 2: "round_cap", 3: "log_overflow", 4: "internal",
-                      5: "anomaly"}
+                      6: "reference_error"}
 
 SS_POLICY = {"semantic": 0, "fcfs": 1, "sjf": 2, "hpjf": 3}
 SS_FLAG_ROUND_LOG = 1

@@ -52,7 +52,7 @@ struct __align__(16) MemS {
 
 struct WarpSmem {
     Key F[FCAP];    // sorted queue front
-    Key X[32];      // scratch keys (ongoing keys / insert ranking / refill)
+    Key X[64];      // scratch keys (pool ranking: candidates 0..31, ongoing 32..63)
     MemS M[32];     // member hand-off between lanes
 };
 
@@ -325,27 +325,76 @@ __device__ __forceinline__ void log_put(Trace& T, long long pos, uint32_t v) {
     if (T.log && pos < T.logcap) T.log[pos] = v;
 }
 
-// ---- eviction -------------------------------------------------------------
+__device__ __forceinline__ Key* INS(const KArgs& A) { return reinterpret_cast<Key*>(A.w.ins); }
+__device__ __forceinline__ bool keq(const Key& a, const Key& b) { return a.hi == b.hi && a.lo == b.lo; }
 
 struct Round {
-    unsigned G;          // granted batch positions
-    unsigned evmask;     // positions evicted with a recorded decision
-    int ndec;            // recorded decisions this round
+    unsigned G;                // granted batch positions
+    unsigned evmask;           // positions evicted with a recorded decision
+    int ndec;                  // recorded decisions this round
     unsigned long long dpend;  // digest terms of the current eviction call (lane 0)
     unsigned long long rmF;    // FRONT entries to drop at the rebuild
 };
 
+__device__ __forceinline__ void set_status(Trace& T, int st) {
+    if (T.status == SS_TRACE_OK) T.status = st;
+}
 
-// Evict one victim for member `kslot`; returns false if none is evictable.
-// `mem` is the caller lane's batch member (refreshed if it is the victim).
+// Index of slot v's live entry in this round's re-queue list, or -1.
+__device__ int ins_find(const KArgs& A, const Trace& T, uint32_t v, int lane) {
+    for (int base = 0; base < T.nins; base += 32) {
+        int i = base + lane;
+        bool hit = i < T.nins && (INS(A)[T.off + i].aux & SLOT_MASK) == v;
+        unsigned hm = __ballot_sync(FULL, hit);
+        if (hm) return base + __ffs(hm) - 1;
+    }
+    return -1;
+}
+
+// heap.delete_by_id for a queued request (heaps.py:67-70): FRONT, BACK or the
+// pending re-queue list. Caller updates the flags.
+__device__ void q_delete(const Env& E, Trace& T, Round& R, uint32_t v, uint32_t flg) {
+    const KArgs& A = *E.A;
+    WarpSmem* sm = E.sm;
+    const int lane = E.lane;
+    if (!(flg & F_Q)) return;
+    if (flg & F_INS) {
+        int idx = ins_find(A, T, v, lane);
+        if (idx >= 0 && lane == 0) INS(A)[T.off + idx].aux = SLOT_MASK;  // dead entry
+        __syncwarp();
+        return;
+    }
+    bool f0 = lane < T.nF && !((R.rmF >> lane) & 1ull) && (sm->F[lane].aux & SLOT_MASK) == v;
+    bool f1 = lane + 32 < T.nF && !((R.rmF >> (lane + 32)) & 1ull) && (sm->F[lane + 32].aux & SLOT_MASK) == v;
+    unsigned m0 = __ballot_sync(FULL, f0), m1 = __ballot_sync(FULL, f1);
+    if (m0 | m1) {
+        if (m0) R.rmF |= 1ull << (__ffs(m0) - 1);
+        else R.rmF |= 1ull << (32 + __ffs(m1) - 1);
+        return;
+    }
+    int found = -1;
+    for (int base = 0; base < T.nB && found < 0; base += 32) {
+        int i = base + lane;
+        bool hit = i < T.nB && (BK(A)[T.off + i].aux & SLOT_MASK) == v;
+        unsigned hm = __ballot_sync(FULL, hit);
+        if (hm) found = base + __ffs(hm) - 1;
+    }
+    if (found >= 0) {
+        if (lane == 0) BK(A)[T.off + found] = BK(A)[T.off + T.nB - 1];
+        T.nB -= 1;
+    }
+    __syncwarp();
+}
+
+// Evict one victim for member `kslot` (kvcache.py:160-175): the resident with
+// the largest dispatch key that is neither granted this round nor `kslot`.
+// Returns false if there is none (AdmissionFailure).
 template <int POL>
 __device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int m, MemS& mem,
                           unsigned& vcall) {
     const KArgs& A = *E.A;
-    WarpSmem* sm = E.sm;
     const int lane = E.lane;
     const ss_profile& P = A.P.profile;
-    // arg-max of the dispatch key over residents that are not protected
     Key best;
     bool have = false;
     int best_ri = -1;
@@ -380,7 +429,7 @@ __device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int 
     if (!have) return false;
     const uint32_t v = best.aux & SLOT_MASK;
     const long long gv = T.off + v;
-    // ---- should_recompute (kvcache.py:81-134), computed redundantly per lane
+    // ---- should_recompute (kvcache.py:81-134), evaluated redundantly per lane
     uint32_t prompt = __ldg(A.in.prompt_len + gv), mid = __ldg(A.in.pred_len + gv);
     uint32_t dec = A.w.dec[gv], flg = A.w.flg[gv];
     double ftb = A.w.ft[gv];
@@ -402,47 +451,23 @@ __device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int 
     long long kvh = psaved + saved;
     double fta = remaining_time(prompt, mid, pf ? prompt : 0, saved, kvh, P);
     T.used -= freed;
-    // where is it? batch member (by lane), pushed-back/ins, FRONT, BACK
-    unsigned bpos = __ballot_sync(FULL, lane < m && mem.slot == v);
-    uint32_t nflg = (flg & ~(F_STAGE | F_PF)) | ST_WAIT | (pf ? F_PF : 0u);
-    if ((flg & F_Q) && !(flg & F_INS)) {
-        // in FRONT or BACK: delete by slot
-        bool f0 = lane < T.nF && (sm->F[lane].aux & SLOT_MASK) == v;
-        bool f1 = lane + 32 < T.nF && (sm->F[lane + 32].aux & SLOT_MASK) == v;
-        unsigned m0 = __ballot_sync(FULL, f0), m1 = __ballot_sync(FULL, f1);
-        if (m0 | m1) {
-            if (m0) R.rmF |= 1ull << (__ffs(m0) - 1);
-            else R.rmF |= 1ull << (32 + __ffs(m1) - 1);
-        } else {
-            int found = -1;
-            for (int base = 0; base < T.nB && found < 0; base += 32) {
-                int i = base + lane;
-                bool hit = i < T.nB && (BK(A)[T.off + i].aux & SLOT_MASK) == v;
-                unsigned hm = __ballot_sync(FULL, hit);
-                if (hm) found = base + __ffs(hm) - 1;
-            }
-            if (found >= 0) {
-                if (lane == 0) BK(A)[T.off + found] = BK(A)[T.off + T.nB - 1];
-                T.nB -= 1;
-            }
-        }
-        nflg &= ~F_Q;
-    }
-    const bool add_ins = !(nflg & F_INS);
+    const Key nkey = make_key<POL>(__ldg(A.in.pred_urgency + gv), fta, __ldg(A.in.tie_rank + gv), v, false);
+    // heap: delete_by_id if queued, then insert with the new key
+    int ins_idx = -1;
+    if ((flg & F_Q) && (flg & F_INS)) ins_idx = ins_find(A, T, v, lane);
+    else q_delete(E, T, R, v, flg);
+    uint32_t nflg = (flg & ~(F_STAGE | F_PF)) | ST_WAIT | (pf ? F_PF : 0u) | F_Q | F_INS;
     if (lane == 0) {
-        // release the resident slot (swap-remove)
-        uint32_t last = A.w.R[T.off + T.nR - 1];
+        uint32_t last = A.w.R[T.off + T.nR - 1];  // resident list: swap-remove
         A.w.R[T.off + best_ri] = last;
         A.w.rpos[T.off + last] = (uint32_t)best_ri;
-        // state write-back
-        if (add_ins) A.w.ins[T.off + T.nins] = v;
-        nflg |= F_Q | F_INS;
+        if (ins_idx >= 0) INS(A)[T.off + ins_idx] = nkey;
+        else INS(A)[T.off + T.nins] = nkey;
         A.w.flg[gv] = nflg;
         A.w.dec[gv] = (uint32_t)saved;
         A.w.ft[gv] = fta;
         A.out.req.evictions[gv] += 1u;
-        // decision record (logged / digested only if the call succeeds)
-        int d = R.ndec;
+        int d = R.ndec;  // decision record: kept only if the admission succeeds
         if (T.log) {
             long long p = T.logpos + SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * d;
             unsigned long long fb = dbits(ftb), fa = dbits(fta);
@@ -466,15 +491,14 @@ __device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int 
             R.dpend += ss_term(r, SS_TAG_EV4, d, dbits(fta));
         }
     }
-    if (add_ins) T.nins += 1;
+    if (ins_idx < 0) T.nins += 1;
     T.nR -= 1;
     R.ndec += 1;
     __syncwarp();
-    if (bpos) {
-        int p = __ffs(bpos) - 1;
-        vcall |= 1u << p;
-        if (lane == p) load_mem(A, T.off, v, mem);
-    }
+    // every batch copy of the victim is skipped (evicted_ids is by id) and refreshed
+    unsigned bpos = __ballot_sync(FULL, lane < m && mem.slot == v);
+    vcall |= bpos;
+    if ((bpos >> lane) & 1u) load_mem(A, T.off, v, mem);
     __syncwarp();
     return true;
 }
@@ -495,10 +519,6 @@ __device__ __forceinline__ MemQ mem_q(const MemS& m) {
     long long e = (long long)m.prompt + m.mid - q.kvd;
     q.est = e > 0 ? e : 0;
     return q;
-}
-
-__device__ __forceinline__ void set_status(Trace& T, int st) {
-    if (T.status == SS_TRACE_OK) T.status = st;
 }
 
 // --------------------------------------------------------------------------
@@ -536,13 +556,14 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
         T.logpos = 0;
         T.log = nullptr;
         T.logcap = 0;
+        bool anom = false;  // a stale heap entry may exist: general (exact) round path
         if ((A.P.flags & SS_FLAG_ROUND_LOG) && A.out.round_log && A.out.log_offsets) {
             T.log = A.out.round_log + A.out.log_offsets[t];
             T.logcap = A.out.log_offsets[t + 1] - A.out.log_offsets[t];
         }
         unsigned long long dig = 0ull;
 
-        // ---- init (engine.py:183-199): f_t, pre-filter, pending list
+        // ---- init (engine.py:183-199): f_t, unservable pre-filter, pending list
         T.npend = 0;
         for (int base = 0; base < T.n; base += 32) {
             int i = base + lane;
@@ -553,12 +574,11 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 uint32_t prompt = A.in.prompt_len[g], mid = A.in.pred_len[g];
                 A.w.ft[g] = remaining_time(prompt, mid, 0, 0, 0, P);
                 A.w.dec[g] = 0u;
-                A.w.flg[g] = ST_WAIT;
                 A.out.req.first_scheduled[g] = __longlong_as_double(0x7ff8000000000000ll);
                 A.out.req.finish_time[g] = __longlong_as_double(0x7ff8000000000000ll);
                 A.out.req.evictions[g] = 0u;
                 serv = (long long)prompt + 1 <= T.cap;
-                if (!serv) A.w.flg[g] = ST_UNS;
+                A.w.flg[g] = serv ? ST_WAIT : ST_UNS;
             }
             unsigned sm_ = __ballot_sync(FULL, v && serv), um = __ballot_sync(FULL, v && !serv);
             if (v && serv) A.w.pend[T.off + T.npend + __popc(sm_ & lt)] = (uint32_t)i;
@@ -569,8 +589,8 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
         T.cursor = 0;
         __syncwarp();
 
-        MemS om;          // ongoing member held by this lane (lane < nO)
-        Key okey;         // its dispatch key
+        MemS om;   // ongoing member copy held by this lane (lane < nO)
+        Key okey;  // its dispatch key
         om.slot = 0;
 
         // ---- the round loop (engine.py:202-224)
@@ -588,8 +608,7 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                         ok = A.in.ready_time[T.off + s] <= thr;
                     }
                     unsigned am = __ballot_sync(FULL, ok);
-                    int cnt = __ffs(~am) - 1;
-                    if (am == FULL) cnt = 32;
+                    int cnt = am == FULL ? 32 : __ffs(~am) - 1;
                     if (cnt == 0) break;
                     bool mine = lane < cnt;
                     Key k;
@@ -615,81 +634,143 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
             const int nc = T.nF < b ? T.nF : b;
             const bool has_c = lane < nc;
             const bool has_o = lane < T.nO;
-            Key ck;
+            Key ck;   // candidate's key: stored (fast path) or current (general path)
             MemS cm;
             if (has_c) {
                 ck = sm->F[lane];
-                load_mem(A, T.off, ck.aux & SLOT_MASK, cm);  // prefetch, used if selected
+                load_mem(A, T.off, ck.aux & SLOT_MASK, cm);  // used if selected
+                if (anom) ck = make_key<POL>(cm.urank, cm.ft, cm.tie, cm.slot, (cm.flg & F_STAGE) == ST_DEC);
             }
-            // p* = min(C[0], min ongoing)
-            Key omin = has_o ? okey : kinf();
+            // p* = min over candidates and ongoing (current keys)
+            Key pmin = has_o ? okey : kinf();
+            if (anom || lane == 0) {
+                if (has_c && klt(ck, pmin)) pmin = ck;
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                Key x = kshfl_xor(omin, o);
-                if (klt(x, omin)) omin = x;
+                Key x = kshfl_xor(pmin, o);
+                if (klt(x, pmin)) pmin = x;
             }
-            bool pstar_prefill;
-            if (nc > 0 && (T.nO == 0 || klt(sm->F[0], omin))) pstar_prefill = !(sm->F[0].aux & DEC_BIT);
-            else pstar_prefill = false;
+            const bool pstar_prefill = !(pmin.aux & DEC_BIT);
             const int kind = pstar_prefill ? SS_KIND_PREFILL : SS_KIND_DECODE;
             const bool c_elig = has_c && (pstar_prefill || (ck.aux & DEC_BIT));
             const unsigned cmask = __ballot_sync(FULL, c_elig);
-            if (has_o) sm->X[lane] = okey;
-            __syncwarp();
             int cnt_c = 0, cnt_o = 0;
-            for (int k = 0; k < T.nO; k++) {
-                Key x = sm->X[k];
-                if (c_elig && klt(x, ck)) cnt_c++;
-                if (has_o && klt(x, okey)) cnt_o++;
-            }
-            if (has_o) {
-                int lo = 0, hi = nc;
-                while (lo < hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (klt(sm->F[mid], okey)) lo = mid + 1;
-                    else hi = mid;
+            if (!anom) {
+                // candidates are FRONT[0..nc), already sorted: merge by rank
+                if (has_o) sm->X[32 + lane] = okey;
+                __syncwarp();
+                for (int k = 0; k < T.nO; k++) {
+                    Key x = sm->X[32 + k];
+                    if (c_elig && klt(x, ck)) cnt_c++;
+                    if (has_o && klt(x, okey)) cnt_o++;
                 }
-                unsigned below = lo >= 32 ? FULL : ((1u << lo) - 1u);
-                cnt_o += __popc(cmask & below);
+                if (has_o) {
+                    int lo = 0, hi = nc;
+                    while (lo < hi) {
+                        int mid = (lo + hi) >> 1;
+                        if (klt(sm->F[mid], okey)) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    unsigned below = lo >= 32 ? FULL : ((1u << lo) - 1u);
+                    cnt_o += __popc(cmask & below);
+                }
+                cnt_c += __popc(cmask & lt);
+            } else {
+                // general: stable sort of (candidates + ongoing) by current key;
+                // equal keys are copies of one request, ordered by pool position
+                if (c_elig) sm->X[lane] = ck;
+                if (has_o) sm->X[32 + lane] = okey;
+                __syncwarp();
+                for (int k = 0; k < nc; k++) {
+                    if (!((cmask >> k) & 1u)) continue;
+                    Key x = sm->X[k];
+                    if (c_elig && (klt(x, ck) || (keq(x, ck) && k < lane))) cnt_c++;
+                    if (has_o && (klt(x, okey) || keq(x, okey))) cnt_o++;
+                }
+                for (int k = 0; k < T.nO; k++) {
+                    Key x = sm->X[32 + k];
+                    if (c_elig && klt(x, ck)) cnt_c++;
+                    if (has_o && (klt(x, okey) || (keq(x, okey) && k < lane))) cnt_o++;
+                }
             }
-            const int c_rank = __popc(cmask & lt) + cnt_c;
+            const int c_rank = cnt_c;
             const int elig = __popc(cmask) + T.nO;
             const int m = elig < b ? elig : b;
+            const bool c_sel = c_elig && c_rank < m;
+            Round R;
+            R.G = 0;
+            R.evmask = 0;
+            R.ndec = 0;
+            R.dpend = 0ull;
+            R.rmF = (unsigned long long)__ballot_sync(FULL, c_sel);
             __syncwarp();
-            if (c_elig && c_rank < m) {
+            if (c_sel) {
                 // popped from the heap for good: no longer queued
                 cm.flg &= ~F_Q;
                 A.w.flg[T.off + cm.slot] = cm.flg;
                 sm->M[c_rank] = cm;
             }
             if (has_o && cnt_o < m) sm->M[cnt_o] = om;
-            bool pushed_o = has_o && cnt_o >= m;   // merged[b:] from ongoing -> heap
-            __syncwarp();
-            MemS mem;
-            mem.slot = 0;
-            if (lane < m) mem = sm->M[lane];
-            Round R;
-            R.G = 0;
-            R.evmask = 0;
-            R.ndec = 0;
-            R.dpend = 0ull;
-            R.rmF = (unsigned long long)__ballot_sync(FULL, c_elig && c_rank < m);
-            // pushed-back ongoing members go back to the queue
-            {
-                unsigned pm = __ballot_sync(FULL, pushed_o);
-                if (pushed_o) {
-                    long long g = T.off + om.slot;
-                    A.w.flg[g] = om.flg | F_Q | F_INS;
-                    A.w.ins[T.off + T.nins + __popc(pm & lt)] = om.slot;
+            if (anom) {
+                // candidates not selected are pushed back with their current key;
+                // a stale stored key is replaced (heaps.py insert after pop)
+                bool refresh = has_c && !c_sel && !keq(ck, sm->F[lane]);
+                unsigned rm2 = __ballot_sync(FULL, refresh);
+                R.rmF |= (unsigned long long)rm2;
+                if (refresh) {
+                    INS(A)[T.off + T.nins + __popc(rm2 & lt)] = ck;
+                    A.w.flg[T.off + cm.slot] = cm.flg | F_INS;
+                }
+                T.nins += __popc(rm2);
+                __syncwarp();
+                // pushed-back ongoing copies: inserting an id already queued is a
+                // DuplicateRequestError in the reference (heaps.py:49-51)
+                unsigned pm = __ballot_sync(FULL, has_o && cnt_o >= m);
+                while (pm) {
+                    int k = __ffs(pm) - 1;
+                    pm &= pm - 1;
+                    uint32_t s = __shfl_sync(FULL, om.slot, k);
+                    uint32_t f = A.w.flg[T.off + s];
+                    if (f & F_Q) {
+                        set_status(T, SS_TRACE_REF_ERROR);
+                        break;
+                    }
+                    Key kk = kshfl(okey, k);
+                    if (lane == 0) {
+                        A.w.flg[T.off + s] = f | F_Q | F_INS;
+                        INS(A)[T.off + T.nins] = kk;
+                    }
+                    T.nins += 1;
+                    __syncwarp();
+                }
+            } else {
+                bool pushed = has_o && cnt_o >= m;
+                unsigned pm = __ballot_sync(FULL, pushed);
+                if (pushed) {
+                    A.w.flg[T.off + om.slot] = om.flg | F_Q | F_INS;
+                    INS(A)[T.off + T.nins + __popc(pm & lt)] = okey;
                 }
                 T.nins += __popc(pm);
             }
+            __syncwarp();
+            if (T.status != SS_TRACE_OK) break;
+            MemS mem;
+            mem.slot = 0xFFFFFFFFu;
+            const bool act = lane < m;
+            if (act) {
+                mem = sm->M[lane];
+                if (anom) mem.flg = A.w.flg[T.off + mem.slot];  // queued bit may have moved
+            }
             const int nO_start = T.nO;
             const int nuns_start = T.nuns;
-            __syncwarp();
+            // a completed request popped from a stale entry: estimate_kv_size raises
+            if (__ballot_sync(FULL, act && (mem.flg & F_STAGE) == ST_DONE)) {
+                set_status(T, SS_TRACE_REF_ERROR);
+                break;
+            }
 
             // ---- admission with KV budget (engine.py:296-327)
-            const bool act = lane < m;
             MemQ q = mem_q(mem);
             {
                 long long inc = act ? q.imm : 0;
@@ -699,14 +780,21 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 bool need = act && (dem + excl + T.used > T.cap);
                 unsigned nm = __ballot_sync(FULL, need);
                 const unsigned mmask = m >= 32 ? FULL : ((1u << m) - 1u);
-                if (nm == 0) {
-                    R.G = mmask;
-                } else {
+                const int f = nm ? __ffs(nm) - 1 : m;
+                R.G = f >= 32 ? FULL : ((1u << f) - 1u);
+                R.G &= mmask;
+                {
+                    // grants of still-queued requests (stale heap entry) before f
+                    unsigned qa = __ballot_sync(FULL, ((R.G >> lane) & 1u) && (mem.flg & F_Q));
+                    if (qa) {
+                        T.anomalies += __popc(qa);
+                        anom = true;
+                    }
+                }
+                if (nm) {
                     // slow path: one member at a time from the first that must evict
-                    int f = __ffs(nm) - 1;
-                    R.G = (1u << f) - 1u;
                     long long reserved = __shfl_sync(FULL, excl, f);
-                    if (act && lane < f) {
+                    if ((R.G >> lane) & 1u) {
                         mem.flg |= F_GRANT;
                         A.w.flg[T.off + mem.slot] = mem.flg;
                     }
@@ -714,16 +802,14 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                     for (int k = f; k < m && T.status == SS_TRACE_OK; k++) {
                         if ((R.evmask >> k) & 1u) continue;
                         q = mem_q(mem);
-                        long long imm_k = __shfl_sync(FULL, q.imm, k);
-                        long long est_k = __shfl_sync(FULL, q.est, k);
-                        long long kvd_k = __shfl_sync(FULL, q.kvd, k);
-                        uint32_t slot_k = __shfl_sync(FULL, mem.slot, k);
-                        uint32_t flg_k = __shfl_sync(FULL, mem.flg, k);
-                        const bool isdec_k = __shfl_sync(FULL, (int)q.isdec, k) != 0;
+                        const long long imm_k = __shfl_sync(FULL, q.imm, k);
+                        const long long est_k = __shfl_sync(FULL, q.est, k);
+                        const long long kvd_k = __shfl_sync(FULL, q.kvd, k);
+                        const uint32_t slot_k = __shfl_sync(FULL, mem.slot, k);
                         long long dem_k = est_k > imm_k ? est_k : imm_k;
                         if (dem_k + reserved > T.cap) dem_k = imm_k;
-                        long long demand = dem_k + reserved;
-                        int d0 = R.ndec;
+                        const long long demand = dem_k + reserved;
+                        const int d0 = R.ndec;
                         unsigned vcall = 0;
                         R.dpend = 0ull;
                         bool ok = true;
@@ -733,17 +819,18 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                                 break;
                             }
                         }
+                        const uint32_t flg_k = __shfl_sync(FULL, mem.flg, k);
                         if (!ok) {
-                            // AdmissionFailure: evictions stand, decisions are lost
+                            // AdmissionFailure: evictions stand, their records are lost
                             T.lost += R.ndec - d0;
                             R.ndec = d0;
-                            // re-read member k (it may not have changed)
-                            flg_k = __shfl_sync(FULL, mem.flg, k);
                             if (kvd_k + imm_k > T.cap) {
                                 // _mark_unservable (engine.py:402-412)
+                                q_delete(E, T, R, slot_k, flg_k);
+                                const bool isdec_k = (flg_k & F_STAGE) == ST_DEC;
                                 if (lane == k) {
                                     long long g = T.off + mem.slot;
-                                    if (q.isdec) {
+                                    if (isdec_k) {
                                         uint32_t ri = A.w.rpos[g];
                                         uint32_t last = A.w.R[T.off + T.nR - 1];
                                         A.w.R[T.off + ri] = last;
@@ -756,13 +843,20 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                                 if (isdec_k) T.nR -= 1;
                                 T.used -= kvd_k;
                                 T.nuns += 1;
+                                __syncwarp();
+                                // other batch copies of it see the new state
+                                if (lane != k && act && mem.slot == slot_k) mem.flg = A.w.flg[T.off + slot_k];
                             } else if (!(flg_k & F_Q)) {
+                                Key kk;
                                 if (lane == k) {
+                                    kk = make_key<POL>(mem.urank, mem.ft, mem.tie, mem.slot, q.isdec);
                                     mem.flg |= F_Q | F_INS;
                                     A.w.flg[T.off + mem.slot] = mem.flg;
-                                    A.w.ins[T.off + T.nins] = mem.slot;
+                                    INS(A)[T.off + T.nins] = kk;
                                 }
                                 T.nins += 1;
+                                __syncwarp();
+                                if (lane != k && act && mem.slot == slot_k) mem.flg = A.w.flg[T.off + slot_k];
                             }
                             __syncwarp();
                             continue;
@@ -771,10 +865,10 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                         R.evmask |= vcall;
                         if (lane == 0) dig += R.dpend;
                         if (flg_k & F_Q) {
-                            // granted while still queued: the reference keeps a stale
-                            // heap entry for it -- not emulated
+                            // granted while it still has a heap entry (a victim whose
+                            // decision was lost): the reference keeps that stale entry
                             T.anomalies += 1;
-                            set_status(T, SS_TRACE_ANOMALY);
+                            anom = true;
                         }
                         R.G |= 1u << k;
                         reserved += imm_k;
@@ -783,6 +877,7 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                             A.w.flg[T.off + mem.slot] = mem.flg;
                         }
                         __syncwarp();
+                        if (act && lane != k && mem.slot == slot_k) mem.flg |= F_GRANT;
                     }
                 }
             }
@@ -790,17 +885,15 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
             T.evictions += R.ndec;
             const bool g_act = (R.G >> lane) & 1u;
             const int ng = __popc(R.G);
-            unsigned long long r64 = (unsigned long long)T.rounds;
+            const unsigned long long r64 = (unsigned long long)T.rounds;
 
             if (ng == 0) {
                 // nothing granted (engine.py:329-344): clock does not advance
                 T.nO = 0;
-                if (A.P.flags & SS_FLAG_DIGEST) {
-                    if (lane == 0) {
-                        dig += ss_term(r64, SS_TAG_HDR, 0, ss_hdr_word(SS_KIND_NONE, 0, 0, R.ndec));
-                        dig += ss_term(r64, SS_TAG_MEM, 0, (unsigned long long)T.used);
-                        dig += ss_term(r64, SS_TAG_TIME, 0, dbits(T.clock));
-                    }
+                if ((A.P.flags & SS_FLAG_DIGEST) && lane == 0) {
+                    dig += ss_term(r64, SS_TAG_HDR, 0, ss_hdr_word(SS_KIND_NONE, 0, 0, R.ndec));
+                    dig += ss_term(r64, SS_TAG_MEM, 0, (unsigned long long)T.used);
+                    dig += ss_term(r64, SS_TAG_TIME, 0, dbits(T.clock));
                 }
                 if (R.ndec > 0) {
                     if (T.used > T.peak) T.peak = T.used;
@@ -822,10 +915,10 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 T.rounds += 1;
                 if (R.ndec == 0 && T.nuns == nuns_start && nO_start == 0) set_status(T, SS_TRACE_LIVELOCK);
             } else {
-                // ---- batch_duration (engine.py:126-149) over granted members
+                // ---- batch_duration (engine.py:126-149) over granted copies
                 q = mem_q(mem);
                 double total = 0.0;
-                unsigned pre = __ballot_sync(FULL, g_act && !q.isdec);
+                const unsigned pre = __ballot_sync(FULL, g_act && !q.isdec);
                 if (pre) {
                     double rl = reload_time(q.kvh, P);
                     double pft = prefill_time((long long)mem.prompt - q.pfn, P);
@@ -837,7 +930,7 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                         }
                     }
                 }
-                unsigned dm = __ballot_sync(FULL, g_act && q.isdec);
+                const unsigned dm = __ballot_sync(FULL, g_act && q.isdec);
                 if (dm) {
                     double st = (g_act && q.isdec)
                                     ? decode_step_time((long long)mem.prompt + mem.dec + 1, 1, P)
@@ -861,41 +954,44 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 const double end = ss::add(T.clock, total);
 
                 // ---- per-member progress (engine.py:351-363, 382-421)
-                long long delta = 0;
-                bool done = false, newres = false;
-                if (g_act) {
-                    long long g = T.off + mem.slot;
-                    if (!(mem.flg & F_FIRST)) {
-                        A.out.req.first_scheduled[g] = T.clock;
-                        mem.flg |= F_FIRST;
+                bool done = false;
+                const unsigned dupm = __match_any_sync(FULL, g_act ? mem.slot : (0x80000000u | lane));
+                const bool dups = __ballot_sync(FULL, g_act && __popc(dupm) > 1) != 0;
+                if (!dups) {
+                    long long delta = 0;
+                    bool newres = false;
+                    if (g_act) {
+                        long long g = T.off + mem.slot;
+                        if (!(mem.flg & F_FIRST)) {
+                            A.out.req.first_scheduled[g] = T.clock;
+                            mem.flg |= F_FIRST;
+                        }
+                        if (q.isdec) {
+                            delta = 1;
+                            mem.dec += 1;
+                        } else {
+                            delta = q.kvh + ((long long)mem.prompt - q.pfn);
+                            mem.flg = (mem.flg & ~F_STAGE) | ST_DEC | F_PF;
+                            newres = true;
+                        }
+                        mem.flg &= ~F_GRANT;
+                        if (mem.dec >= mem.tout) {
+                            done = true;
+                            delta -= (long long)mem.prompt + mem.dec;
+                            A.out.req.finish_time[g] = end;
+                            mem.ft = 0.0;
+                            mem.flg = (mem.flg & ~F_STAGE) | ST_DONE;
+                        } else {
+                            mem.ft = remaining_time(mem.prompt, mem.mid, mem.prompt, mem.dec, 0, P);
+                        }
+                        A.w.dec[g] = mem.dec;
+                        A.w.ft[g] = mem.ft;
+                        A.w.flg[g] = mem.flg;
                     }
-                    if (q.isdec) {
-                        delta = 1;
-                        mem.dec += 1;
-                    } else {
-                        delta = q.kvh + ((long long)mem.prompt - q.pfn);
-                        mem.flg = (mem.flg & ~F_STAGE) | ST_DEC | F_PF;
-                        newres = true;
-                    }
-                    mem.flg &= ~F_GRANT;
-                    if (mem.dec >= mem.tout) {
-                        done = true;
-                        delta -= (long long)mem.prompt + mem.dec;
-                        A.out.req.finish_time[g] = end;
-                        mem.ft = 0.0;
-                        mem.flg = (mem.flg & ~F_STAGE) | ST_DONE;
-                    } else {
-                        mem.ft = remaining_time(mem.prompt, mem.mid, mem.prompt, mem.dec, 0, P);
-                    }
-                    A.w.dec[g] = mem.dec;
-                    A.w.ft[g] = mem.ft;
-                    A.w.flg[g] = mem.flg;
-                }
-                T.used += warp_sum_ll(delta);
-                if (T.used > T.cap || T.used < 0) set_status(T, SS_TRACE_INTERNAL);
-                // resident list: newly prefilled join, completed leave
-                {
-                    unsigned nm = __ballot_sync(FULL, newres);
+                    // allocations all fit (admission reserved them); completions release
+                    T.used += warp_sum_ll(delta);
+                    if (T.used > T.cap || T.used < 0) set_status(T, SS_TRACE_INTERNAL);
+                    const unsigned nm = __ballot_sync(FULL, newres);
                     if (newres) {
                         uint32_t idx = (uint32_t)(T.nR + __popc(nm & lt));
                         A.w.R[T.off + idx] = mem.slot;
@@ -916,6 +1012,89 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                         }
                         T.nR -= 1;
                         __syncwarp();
+                    }
+                } else {
+                    // duplicate copies of a request: execute copies one by one,
+                    // each seeing the previous copy's effect
+                    unsigned gm = R.G;
+                    while (gm && T.status == SS_TRACE_OK) {
+                        int k = __ffs(gm) - 1;
+                        gm &= gm - 1;
+                        int err = 0, dn = 0, nres = 0;
+                        long long alloc = 0, rel = 0;
+                        if (lane == k) {
+                            long long g = T.off + mem.slot;
+                            uint32_t dec = A.w.dec[g], fl = A.w.flg[g];
+                            if ((fl & F_STAGE) == ST_DONE) {
+                                err = 1;  // transition(PREFILLING) from COMPLETED
+                            } else {
+                                if (!(fl & F_FIRST)) {
+                                    A.out.req.first_scheduled[g] = T.clock;
+                                    fl |= F_FIRST;
+                                }
+                                if ((fl & F_STAGE) == ST_DEC) {
+                                    alloc = 1;
+                                    dec += 1;
+                                } else {
+                                    long long pfn = (fl & F_PF) ? (long long)mem.prompt : 0;
+                                    alloc = pfn + dec + ((long long)mem.prompt - pfn);
+                                    fl = (fl & ~F_STAGE) | ST_DEC | F_PF;
+                                    nres = 1;
+                                }
+                                fl &= ~F_GRANT;
+                                double ft;
+                                if (dec >= mem.tout) {
+                                    dn = 1;
+                                    rel = (long long)mem.prompt + dec;
+                                    A.out.req.finish_time[g] = end;
+                                    ft = 0.0;
+                                    fl = (fl & ~F_STAGE) | ST_DONE;
+                                } else {
+                                    ft = remaining_time(mem.prompt, mem.mid, mem.prompt, dec, 0, P);
+                                }
+                                A.w.dec[g] = dec;
+                                A.w.ft[g] = ft;
+                                A.w.flg[g] = fl;
+                            }
+                        }
+                        err = __shfl_sync(FULL, err, k);
+                        dn = __shfl_sync(FULL, dn, k);
+                        nres = __shfl_sync(FULL, nres, k);
+                        alloc = __shfl_sync(FULL, alloc, k);
+                        rel = __shfl_sync(FULL, rel, k);
+                        const uint32_t s = __shfl_sync(FULL, mem.slot, k);
+                        if (err || alloc > T.cap - T.used) {
+                            set_status(T, SS_TRACE_REF_ERROR);
+                            break;
+                        }
+                        T.used += alloc;
+                        if (lane == k) done = dn != 0;
+                        if (lane == 0) {
+                            if (nres) {
+                                A.w.R[T.off + T.nR] = s;
+                                A.w.rpos[T.off + s] = (uint32_t)T.nR;
+                            }
+                        }
+                        if (nres) T.nR += 1;
+                        __syncwarp();
+                        if (dn) {
+                            if (lane == 0) {
+                                uint32_t ri = A.w.rpos[T.off + s];
+                                uint32_t last = A.w.R[T.off + T.nR - 1];
+                                A.w.R[T.off + ri] = last;
+                                A.w.rpos[T.off + last] = ri;
+                            }
+                            T.nR -= 1;
+                            T.used -= rel;
+                        }
+                        __syncwarp();
+                    }
+                    if (T.status != SS_TRACE_OK) break;
+                    if (g_act) {  // every copy sees the final state
+                        long long g = T.off + mem.slot;
+                        mem.dec = A.w.dec[g];
+                        mem.flg = A.w.flg[g];
+                        mem.ft = A.w.ft[g];
                     }
                 }
                 // ---- ITERATION_END record (engine.py:365-380) + digest
@@ -951,8 +1130,8 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 if (T.used > T.peak) T.peak = T.used;
                 T.clock = end;
                 T.rounds += 1;
-                // ---- ongoing = granted and not completed, in granted order
-                const bool stay = g_act && !done;
+                // ---- ongoing = granted copies not completed, in granted order
+                const bool stay = g_act && (mem.flg & F_STAGE) != ST_DONE;
                 const unsigned smk = __ballot_sync(FULL, stay);
                 __syncwarp();
                 if (stay) sm->M[__popc(smk & lt)] = mem;
@@ -966,22 +1145,22 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
             if (T.log && T.logpos > T.logcap) set_status(T, SS_TRACE_LOG_OVERFLOW);
             if (A.P.max_rounds > 0 && T.rounds >= A.P.max_rounds) set_status(T, SS_TRACE_ROUND_CAP);
 
-            // ---- queue rebuild: drop taken FRONT entries, insert pushed-back,
-            //      failed and evicted requests with their current keys
+            // ---- queue rebuild: drop popped FRONT entries, then insert this
+            //      round's pushed-back / failed / evicted requests with the key
+            //      they were queued with (the heap stores keys at insert time)
             f_compact(E, T, R.rmF);
             for (int base = 0; base < T.nins; base += 32) {
                 int i = base + lane;
                 bool v = false;
                 Key k;
                 if (i < T.nins) {
-                    uint32_t s = A.w.ins[T.off + i];
-                    long long g = T.off + s;
-                    uint32_t f = A.w.flg[g];
-                    if (f & F_INS) {
+                    k = INS(A)[T.off + i];
+                    uint32_t s = k.aux & SLOT_MASK;
+                    if (s != SLOT_MASK) {
+                        long long g = T.off + s;
+                        uint32_t f = A.w.flg[g];
                         v = true;
                         A.w.flg[g] = f & ~F_INS;
-                        k = make_key<POL>(__ldg(A.in.pred_urgency + g), A.w.ft[g], __ldg(A.in.tie_rank + g), s,
-                                          (f & F_STAGE) == ST_DEC);
                     }
                 }
                 q_insert32<POL>(E, T, k, v);
@@ -994,7 +1173,6 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
         {
             PySum acc;
             acc.init();
-            int mylv = lane;  // lanes 0..15: per-level normalized wait
             for (int base = 0; base < T.n; base += 32) {
                 int i = base + lane;
                 bool v = i < T.n;
@@ -1006,10 +1184,7 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                     uint32_t f = A.w.flg[g], dcount = A.w.dec[g];
                     A.out.req.generated[g] = dcount;
                     if (A.out.req.f_t) A.out.req.f_t[g] = A.w.ft[g];
-                    if (A.out.req.state) {
-                        uint32_t st = f & F_STAGE;
-                        A.out.req.state[g] = st | ((f & F_PF) ? 256u : 0u);
-                    }
+                    if (A.out.req.state) A.out.req.state[g] = (f & F_STAGE) | ((f & F_PF) ? 256u : 0u);
                     double fi = A.out.req.finish_time[g];
                     if (!isnan(fi)) {
                         fin = true;
@@ -1030,8 +1205,8 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 }
             }
             dig = warp_sum_u64(dig);
-            double val = acc.value();
-            int cntv = acc.n;
+            const double val = acc.value();
+            const int cntv = acc.n;
             __syncwarp();
             ss_trace_stats* st = A.out.stats + t;
             if (lane < SS_MAX_LEVELS) {
@@ -1056,7 +1231,6 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 st->_pad = 0;
                 st->final_clock = T.clock;
             }
-            (void)mylv;
         }
         __syncwarp();
     }
@@ -1069,7 +1243,7 @@ static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 size_t work_bytes(int64_t n) {
     size_t nn = (size_t)(n > 0 ? n : 1);
-    return align16(nn * 8) + 4 * align16(nn * 4) + align16(nn * 16) + 3 * align16(nn * 4) + 16;
+    return align16(nn * 8) + 4 * align16(nn * 4) + 2 * align16(nn * 16) + align16(nn * 4) + 16;
 }
 
 void carve_work(void* base, int64_t n, Work* w) {
@@ -1082,8 +1256,7 @@ void carve_work(void* base, int64_t n, Work* w) {
     w->R = (uint32_t*)p;     p += align16(nn * 4);
     w->B = (void*)p;         p += align16(nn * 16);
     w->pend = (uint32_t*)p;  p += align16(nn * 4);
-    w->ins = (uint32_t*)p;   p += align16(nn * 4);
-    p += align16(nn * 4);
+    w->ins = (void*)p;       p += align16(nn * 16);
     w->next_trace = (int*)p;
 }
 

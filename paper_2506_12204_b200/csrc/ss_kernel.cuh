@@ -18,7 +18,7 @@ struct Work {
     void* B;             // queue BACK: 16-byte packed keys
     uint32_t* R;         // resident list (eviction candidates)
     uint32_t* pend;      // servable requests in pending order
-    uint32_t* ins;       // this round's re-queue list
+    void* ins;           // this round's re-queue list: 16-byte keys
     int* next_trace;     // work counter for persistent warps
 };
 

@@ -68,6 +68,19 @@ def full_decision(d):
 
 ref_engine._decision_obj = full_decision
 
+# The granted list is local to Simulator._execute; the engine passes it to the
+# module-level batch_duration (engine.py:346-347), so observe it there.
+_orig_batch_duration = ref_engine.batch_duration
+_last_granted = []
+
+
+def _observing_batch_duration(batch, p, decode_cost="max"):
+    _last_granted[:] = [r.id for r in batch.members]
+    return _orig_batch_duration(batch, p, decode_cost)
+
+
+ref_engine.batch_duration = _observing_batch_duration
+
 
 class Capture(Simulator):
     """Observe every scheduler round of the unmodified engine."""
@@ -85,12 +98,13 @@ class Capture(Simulator):
 
     def _execute(self, batch):
         n0 = len(self.trace.events)
+        _last_granted.clear()
         super()._execute(batch)
         new = self.trace.events[n0:]
         if new:
             ev = new[0]
-            ids = set(ev.payload["ids"])
-            granted = [r.id for r in self._members if r.id in ids]
+            granted = list(_last_granted) if ev.payload["ids"] else []
+            assert sorted(granted) == ev.payload["ids"]
             self.rounds.append({
                 "kind": (0 if ev.payload.get("kind_detail") == "decode" else 1) if granted else 2,
                 "granted": granted,
@@ -111,11 +125,63 @@ def profile_dict(p):
     return {k: getattr(p, k) for k in ("alpha1", "alpha2", "gamma1", "gamma2", "beta_load", "beta_save")}
 
 
+def _params(cfg):
+    wl = cfg.workload
+    return {
+        "policy": cfg.policy.value,
+        "profile": profile_dict(cfg.gpu_profile()),
+        "profile_name": cfg.profile,
+        "batch_size": cfg.batch_size,
+        "memory_capacity": cfg.memory_capacity,
+        "dependency_rule": cfg.dependency_rule,
+        "decode_batch_cost": cfg.decode_batch_cost,
+        "levels": wl.levels,
+        "seed": cfg.seed,
+        "workload": {"total_requests": wl.total_requests, "gap_s": wl.gap_s,
+                     "concurrent": wl.concurrent, "concurrent_mode": wl.concurrent_mode,
+                     "levels": wl.levels, "prompt_len_range": list(wl.prompt_len_range),
+                     "output_len_range": list(wl.output_len_range), "buckets": wl.buckets,
+                     "max_output_len": wl.max_output_len, "seed": wl.seed},
+        "predictor": {"latency_s": cfg.predictor.latency_s, "batch_size": cfg.predictor.batch_size,
+                      "strategy": cfg.predictor.strategy.value,
+                      "urgency_error": cfg.predictor.urgency_error,
+                      "length_error": cfg.predictor.length_error},
+    }
+
+
+def _inputs(pending, recpos):
+    return {
+        "ready": [r.prediction_ready_time for r in pending],
+        "arrival": [r.arrival_time for r in pending],
+        "prompt": [r.prompt_len for r in pending],
+        "true_out": [r.true_output_len for r in pending],
+        "pred_len": [r.predicted_bucket.representative_len for r in pending],
+        "pred_urg": [r.f_e.rank for r in pending],
+        "true_urg": [r.true_urgency.rank for r in pending],
+        "ids": [r.id for r in pending],
+        "record_pos": [recpos[r.id] for r in pending],
+    }
+
+
 def run_case(name, cfg, arrivals_fn, keep_log):
     arrivals = arrivals_fn()
     sim = Capture(cfg, max_rounds=2_000_000)
     t0 = time.perf_counter()
-    trace = sim.run(arrivals)
+    try:
+        trace = sim.run(arrivals)
+    except Exception as exc:  # the reference itself fails on this trace
+        err = f"{type(exc).__name__}: {exc}"
+        dt = time.perf_counter() - t0
+        reqs = sim.requests
+        pending = sorted(reqs, key=lambda r: (r.prediction_ready_time, r.arrival_time, r.id))
+        print(f"{name:28s} REFERENCE RAISED {err} after {len(sim.rounds)} rounds", flush=True)
+        return {
+            "name": name, "params": _params(cfg),
+            "arrivals": [[r.id, r.arrival_time, r.prompt_len, r.true_output_len, r.true_urgency.rank] for r in reqs],
+            "inputs": _inputs(pending, {r.id: i for i, r in enumerate(reqs)}),
+            "expected": {"ref_error": err, "rounds_before_error": len(sim.rounds)},
+            "ref_seconds": dt,
+        }
     dt = time.perf_counter() - t0
     reqs = sim.requests
     pending = sorted(reqs, key=lambda r: (r.prediction_ready_time, r.arrival_time, r.id))
@@ -154,39 +220,10 @@ def run_case(name, cfg, arrivals_fn, keep_log):
     wl = cfg.workload
     case = {
         "name": name,
-        "params": {
-            "policy": cfg.policy.value,
-            "profile": profile_dict(cfg.gpu_profile()),
-            "profile_name": cfg.profile,
-            "batch_size": cfg.batch_size,
-            "memory_capacity": cfg.memory_capacity,
-            "dependency_rule": cfg.dependency_rule,
-            "decode_batch_cost": cfg.decode_batch_cost,
-            "levels": wl.levels,
-            "seed": cfg.seed,
-            "workload": {"total_requests": wl.total_requests, "gap_s": wl.gap_s,
-                         "concurrent": wl.concurrent, "concurrent_mode": wl.concurrent_mode,
-                         "levels": wl.levels, "prompt_len_range": list(wl.prompt_len_range),
-                         "output_len_range": list(wl.output_len_range), "buckets": wl.buckets,
-                         "max_output_len": wl.max_output_len, "seed": wl.seed},
-            "predictor": {"latency_s": cfg.predictor.latency_s, "batch_size": cfg.predictor.batch_size,
-                          "strategy": cfg.predictor.strategy.value,
-                          "urgency_error": cfg.predictor.urgency_error,
-                          "length_error": cfg.predictor.length_error},
-        },
+        "params": _params(cfg),
         "arrivals": [[r.id, r.arrival_time, r.prompt_len, r.true_output_len, r.true_urgency.rank]
                      for r in reqs],
-        "inputs": {
-            "ready": [r.prediction_ready_time for r in pending],
-            "arrival": [r.arrival_time for r in pending],
-            "prompt": [r.prompt_len for r in pending],
-            "true_out": [r.true_output_len for r in pending],
-            "pred_len": [r.predicted_bucket.representative_len for r in pending],
-            "pred_urg": [r.f_e.rank for r in pending],
-            "true_urg": [r.true_urgency.rank for r in pending],
-            "ids": [r.id for r in pending],
-            "record_pos": [recpos[r.id] for r in pending],
-        },
+        "inputs": _inputs(pending, recpos),
         "expected": {
             "records": [[rec.id, rec.first_scheduled, rec.finish_time, rec.generated_tokens,
                          rec.evictions, rec.prediction_ready] for rec in trace.records],
@@ -351,10 +388,23 @@ def cases_large():
     return out
 
 
+def cases_anomaly():
+    """Tight-memory traces where an admission that fails after evicting
+    leaves a victim that is a later batch member; granting it keeps a stale
+    heap entry (duplicates, stale keys) and sometimes crashes the reference."""
+    out = []
+    for cap, seeds in ((700, (0, 1, 2, 3, 7, 9, 12, 14, 17, 21)), (1500, (8, 20, 32))):
+        for sd in seeds:
+            c = scen(workload=WorkloadSpec(total_requests=300, seed=sd, levels=3), seed=sd, memory_capacity=cap)
+            out.append((f"anom_c{cap}_s{sd}", c, gen_arrivals(c), sd < 4))
+    return out
+
+
 def main():
-    which = sys.argv[1:] or ["small", "large"]
+    which = sys.argv[1:] or ["small", "large", "anomaly"]
+    groups = {"small": cases_small, "large": cases_large, "anomaly": cases_anomaly}
     for group in which:
-        cases = cases_small() if group == "small" else cases_large()
+        cases = groups[group]()
         fixtures = [run_case(*c) for c in cases]
         path = os.path.join(HERE, f"golden_{group}.json.gz")
         with gzip.open(path, "wt", encoding="utf-8") as fh:

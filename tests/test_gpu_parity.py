@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 
 SMALL = [c for c in golden_cases("small") if c["params"]["policy"] == "semantic"]
 LARGE = [c for c in golden_cases("large") if c["params"]["policy"] == "semantic"]
+ANOM = golden_cases("anomaly")
 
 
 @pytest.fixture(scope="module")
@@ -39,6 +40,16 @@ def test_gpu_matches_reference_large(native, case):
     check_against_golden(res, case, batch=batch)
 
 
+@pytest.mark.parametrize("case", ANOM, ids=[c["name"] for c in ANOM])
+def test_gpu_matches_reference_stale_entries(native, case):
+    batch = case_batch(case)
+    res = native.run_host(case_params(case, A.SS_FLAG_DIGEST), batch, want_log=True)
+    if "ref_error" in case["expected"]:
+        assert int(res.stats["status"][0]) == A.SS_TRACE_REF_ERROR
+    else:
+        check_against_golden(res, case, batch=batch)
+
+
 def _seeded_batch(n_traces, total, cfg_kw=None, seed0=0):
     from paper_2506_12204_b200.engine import ScenarioConfig
     from paper_2506_12204_b200.soa import TraceBatch, prepare_trace
@@ -52,21 +63,26 @@ def _seeded_batch(n_traces, total, cfg_kw=None, seed0=0):
     return TraceBatch.concat(parts), cfg
 
 
-def _compare_with_oracle(gpu, cpu):
-    from paper_2506_12204_b200 import _abi as A
-
-    for k in ("status", "rounds", "evictions", "digest", "completed", "unservable", "mem_used_peak",
-              "lost_evictions"):
-        assert np.array_equal(gpu.stats[k], cpu.stats[k]), k
-    assert np.array_equal(gpu.stats["final_clock"].view(np.uint64), cpu.stats["final_clock"].view(np.uint64))
+def _compare_with_oracle(gpu, cpu, batch):
+    """Statuses must agree everywhere; every other field is compared on the
+    traces both finished (a reference exception ends a trace mid-round)."""
+    assert np.array_equal(gpu.stats["status"], cpu.stats["status"]), "status"
+    ok = cpu.stats["status"] == 0
+    for k in ("rounds", "evictions", "digest", "completed", "unservable", "mem_used_peak",
+              "lost_evictions", "anomalies"):
+        assert np.array_equal(gpu.stats[k][ok], cpu.stats[k][ok]), k
+    for k in ("final_clock", "sum_wait", "sum_norm_wait", "level_norm_sum"):
+        assert np.array_equal(gpu.stats[k][ok].view(np.uint64), cpu.stats[k][ok].view(np.uint64)), k
+    assert np.array_equal(gpu.stats["level_count"][ok], cpu.stats["level_count"][ok])
+    sizes = np.diff(batch.offsets)
+    rmask = np.repeat(ok, sizes)
     for k in ("first_scheduled", "finish_time", "f_t"):
-        assert np.array_equal(getattr(gpu, k).view(np.uint64), getattr(cpu, k).view(np.uint64)), k
+        assert np.array_equal(getattr(gpu, k)[rmask].view(np.uint64), getattr(cpu, k)[rmask].view(np.uint64)), k
     for k in ("generated", "evictions"):
-        assert np.array_equal(getattr(gpu, k), getattr(cpu, k)), k
-    # fused statistics: bit-exact CPython-3.12 sums
-    for k in ("sum_wait", "sum_norm_wait", "level_norm_sum"):
-        assert np.array_equal(gpu.stats[k].view(np.uint64), cpu.stats[k].view(np.uint64)), k
-    assert np.array_equal(gpu.stats["level_count"], cpu.stats["level_count"])
+        assert np.array_equal(getattr(gpu, k)[rmask], getattr(cpu, k)[rmask]), k
+    for t in np.nonzero(ok)[0]:
+        assert np.array_equal(gpu.unservable[t], cpu.unservable[t])
+    return int(ok.sum())
 
 
 @pytest.mark.parametrize("capacity", [10**9, 1500, 700])
@@ -78,8 +94,7 @@ def test_gpu_many_traces_vs_oracle(native, capacity):
     p = lambda: make_params(cfg.gpu_profile(), 16, capacity, levels=3, flags=A.SS_FLAG_DIGEST)
     gpu = native.run_host(p(), batch)
     cpu = run_oracle(p(), batch, threads=8)
-    assert (cpu.stats["status"] == 0).all()
-    _compare_with_oracle(gpu, cpu)
+    assert _compare_with_oracle(gpu, cpu, batch) >= batch.n_traces // 2
 
 
 @pytest.mark.parametrize("prof", ["a100_qwen7b", "a5000_qwen7b", "mixed"])
@@ -97,10 +112,7 @@ def test_gpu_batch_sizes_profiles_vs_oracle(native, prof, b):
                                 flags=A.SS_FLAG_DIGEST)
         gpu = native.run_host(p(), batch)
         cpu = run_oracle(p(), batch, threads=8)
-        ok = cpu.stats["status"] == 0
-        assert np.array_equal(gpu.stats["status"][ok], cpu.stats["status"][ok])
-        if ok.all():
-            _compare_with_oracle(gpu, cpu)
+        _compare_with_oracle(gpu, cpu, batch)
 
 
 def test_gpu_round_logs_vs_oracle(native):

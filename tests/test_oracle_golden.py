@@ -13,6 +13,7 @@ from paper_2506_12204_b200 import _abi as A
 
 SMALL = golden_cases("small")
 LARGE = golden_cases("large")
+ANOM = golden_cases("anomaly")
 
 
 @pytest.mark.parametrize("case", SMALL, ids=[c["name"] for c in SMALL])
@@ -50,3 +51,17 @@ def test_oracle_threads_match_serial():
         r = run_oracle(p, multi, threads=3)
         assert len(set(int(x) for x in r.stats["digest"])) == 1
         assert format(int(r.stats["digest"][0]), "016x") == c["expected"]["digest"]
+
+
+@pytest.mark.parametrize("case", ANOM, ids=[c["name"] for c in ANOM])
+def test_oracle_matches_reference_stale_entries(case):
+    """Tight memory: victims whose decisions were lost get granted while still
+    queued (stale heap keys, duplicate batch members). Where the reference
+    raises, the oracle must report SS_TRACE_REF_ERROR."""
+    batch = case_batch(case)
+    res = run_oracle(case_params(case, A.SS_FLAG_DIGEST | A.SS_FLAG_ROUND_LOG), batch)
+    if "ref_error" in case["expected"]:
+        assert int(res.stats["status"][0]) == A.SS_TRACE_REF_ERROR
+        assert int(res.stats["rounds"][0]) == case["expected"]["rounds_before_error"] + 1
+    else:
+        check_against_golden(res, case, batch=batch)
