@@ -1,0 +1,354 @@
+"""Benchmark: scheduler decisions/s on BASELINE.json config B (headline) and
+the other named workloads.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload B|A|D|E|C]
+    python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+    python bench.py --impl reference ...     # the CPU reference arm
+
+A step = one pass of the scheduler hot path over the whole synthetic batch:
+every round of every trace (config B: 4,096 traces x 1,000 requests per GPU,
+weak scaling across ranks). ``value`` is device-timed with inputs resident in
+HBM (L2 flushed between steps); ``e2e`` is the same work through the C-ABI
+host-buffer entry (``ss_run_traces_host``: H2D inputs, kernel, D2H results,
+timed on the host clock). The CPU baseline is the oracle port of the
+reference scheduler (oracle/semsched_oracle.c, C, all host threads) on a
+bounded sample of the same traces; its digests double as a full-size parity
+check of the GPU schedules.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "tests"))
+
+METRIC = "scheduler decisions/sec"
+UNIT = "decisions/s"
+
+WORKLOADS = {
+    "B": dict(desc="config B: 4,096 independent traces x 1,000 requests (generate(WorkloadSpec(total_requests=1000, "
+                   "seed=s))), b=16, ample KV (1e9 slots), a100_qwen7b, exact predictors",
+              traces=4096, requests=1000, capacity=10**9, profile="a100_qwen7b", levels=5),
+    "E": dict(desc="config E: 65,536 traces x 2,000 requests per job (generate(WorkloadSpec(total_requests=2000, "
+                   "seed=s))), b=16, ample KV, a100_qwen7b",
+              traces=65536, requests=2000, capacity=10**9, profile="a100_qwen7b", levels=5),
+    "D": dict(desc="config D shape at scale: 4,096 traces x 1,000 requests, 3 levels, KV budget 2,295 slots "
+                   "(25% of the seed-1 ample peak), a100_qwen7b (offload), heavy eviction",
+              traces=4096, requests=1000, capacity=2295, profile="a100_qwen7b", levels=3),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.p is None:
+            return False
+        time.sleep(0.2)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+        return False
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def build_batch(wl, rank, traces_override=None):
+    from paper_2506_12204_b200.tracegen import generate_batch
+    from paper_2506_12204_b200.workload import WorkloadSpec
+
+    T = traces_override or wl["traces"]
+    seeds = np.arange(rank * T, (rank + 1) * T, dtype=np.int64)
+    spec = WorkloadSpec(total_requests=wl["requests"], levels=wl["levels"])
+    return generate_batch(spec, seeds, pinned=True), T
+
+
+def algorithmic_bytes(stats, n_req):
+    """B_decision summed over rounds + per-trace load/store."""
+    s = lambda k: float(stats[k].astype(np.float64).sum())
+    rounds = s("rounds")
+    per_round = (16 * s("sum_pool") + 16 * s("sum_resident_evict") + 84 * (s("sum_granted") + s("sum_victims"))
+                 + 4 * s("sum_granted") + 4 * s("completed") + 32 * s("sum_victims") + 32 * rounds)
+    return per_round + (28 + 16) * n_req + 80 * len(stats)
+
+
+def cpu_oracle(params_fn, batch, sample, threads):
+    """Time the C oracle (test infrastructure) on the first `sample` traces."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.soa import TraceBatch
+
+    sub = TraceBatch(offsets=batch.offsets[: sample + 1].copy(),
+                     **{f: getattr(batch, f)[: int(batch.offsets[sample])] for f in
+                        ("ready", "arrival", "prompt", "true_out", "pred_len", "pred_urg", "true_urg", "tie",
+                         "ids", "record_pos")})
+    t0 = time.perf_counter()
+    res = run_oracle(params_fn(), sub, threads=threads)
+    dt = time.perf_counter() - t0
+    return res, dt
+
+
+def reference_arm(args, wl):
+    """The reference's CPU scheduler, timed on this box's host cores."""
+    import torch  # noqa: F401  (pinned buffers in generate_batch)
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.results import make_params
+    from paper_2506_12204_b200 import _abi as A
+
+    batch, T = build_batch(wl, 0, args.traces)
+    threads = os.cpu_count() or 1
+    sample = min(T, max(threads * 2, 64))
+    pf = lambda: make_params(get_profile(wl["profile"]), 16, wl["capacity"], levels=wl["levels"], flags=A.SS_FLAG_DIGEST)
+    for _ in range(args.warmup):
+        cpu_oracle(pf, batch, min(sample, threads), threads)
+    times, decs = [], 0
+    for _ in range(args.steps):
+        res, dt = cpu_oracle(pf, batch, sample, threads)
+        times.append(dt)
+        decs = int(res.stats["rounds"].sum())
+    tot = sum(times)
+    value = decs * len(times) / tot
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": wl["desc"], "sample_traces_per_step": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"first {sample} of {T} traces per step (oracle/semsched_oracle.c, "
+                                       f"a C restatement of the reference scheduler), {threads} threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "traces_per_s": sample * len(times) / tot}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="B", choices=sorted(WORKLOADS))
+    ap.add_argument("--traces", type=int, default=None, help="override traces per rank")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return reference_arm(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_12204_b200 import _abi as A
+    from paper_2506_12204_b200 import native
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.results import make_params
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    t0 = time.perf_counter()
+    batch, T = build_batch(wl, rank, args.traces)
+    log(f"[rank {rank}] traces {T} x {wl['requests']} prepared in {time.perf_counter() - t0:.2f} s")
+    prof = get_profile(wl["profile"])
+    pf = lambda: make_params(prof, 16, wl["capacity"], levels=wl["levels"], flags=A.SS_FLAG_DIGEST)
+    dbatch = native.DeviceBatch(batch, dev)
+    douts = native.DeviceOutputs(batch.n_requests, T, dev, with_state=False)
+    ws = native.Workspace(pf(), T, batch.n_requests, dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    gathered = torch.empty(world * T * C.sizeof(A.ss_trace_stats), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        native.run_device(pf(), dbatch, douts, ws, stream=stream)
+        if world > 1:  # the one collective: gather per-trace statistics
+            dist.all_gather_into_tensor(gathered, douts.t["stats"])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stats = douts.stats_numpy()
+    bad = int((stats["status"] != 0).sum())
+    decisions = int(stats["rounds"].sum())
+    cfgk = native.kernel_config(pf(), T)
+
+    # ---- timed region: device events per step, L2 flushed between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    ms_step = float(np.mean(ms))
+    t_total = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+    dec_t = torch.tensor([decisions * args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_total, op=dist.ReduceOp.MAX)
+        dist.all_reduce(dec_t, op=dist.ReduceOp.SUM)
+    value = float(dec_t.item()) / (float(t_total.item()) / 1e3)
+    traces_s = world * T * args.steps / (float(t_total.item()) / 1e3)
+
+    # kernel-only duration (the dominant and only kernel) on the same stream
+    kms = []
+    for _ in range(3):
+        flush.zero_()
+        kms.append(native.run_device(pf(), dbatch, douts, ws, stream=stream, time_kernel=True))
+    k_ms = float(np.mean(kms))
+    n_req = batch.n_requests
+    alg = algorithmic_bytes(stats, n_req)
+    peak, peak_src = measured_peak()
+    achieved = alg / (k_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", f"ncu_traffic_{args.workload}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        if tj.get("traces") == T:
+            traffic = tj.get("dram_bytes_per_launch")
+
+    # ---- end to end through the C-ABI host entry (pinned host buffers)
+    e2e = None
+    if not args.no_e2e:
+        from paper_2506_12204_b200.results import alloc_host_outputs
+
+        hb = native.host_batch(batch)
+        outs = alloc_host_outputs(n_req, T)
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy() if a.size else a
+        outs = {k: pin(v) for k, v in outs.items()}
+        o = A.ss_outputs()
+        o.req = A.ss_request_out(outs["first_scheduled"].ctypes.data, outs["finish_time"].ctypes.data,
+                                 outs["generated"].ctypes.data, outs["evictions"].ctypes.data, None, None)
+        o.stats = outs["stats"].ctypes.data
+        o.unservable_slots = outs["unservable"].ctypes.data
+        h2d = batch.nbytes_inputs()
+        d2h = n_req * (8 + 8 + 4 + 4 + 4) + T * C.sizeof(A.ss_trace_stats)
+        L = native.lib()
+        st = C.c_void_p(stream.cuda_stream)
+        for _ in range(2):
+            L.ss_run_traces_host(C.byref(pf()), C.byref(hb), C.byref(o), st, None)
+        if world > 1:
+            dist.barrier()
+        et = []
+        for _ in range(args.steps):
+            t1 = time.perf_counter()
+            rc = L.ss_run_traces_host(C.byref(pf()), C.byref(hb), C.byref(o), st, None)
+            et.append(time.perf_counter() - t1)
+            assert rc == 0, native.last_error()
+        e_tot = torch.tensor([sum(et)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_tot, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(dec_t.item()) / float(e_tot.item()), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(e_tot.item()) / args.steps}
+
+    # ---- CPU baseline (oracle port) on a bounded sample; digests = parity check
+    cpu = None
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        sample = min(T, max(threads * 2, 64))
+        res, dt = cpu_oracle(pf, batch, sample, threads)
+        cdec = int(res.stats["rounds"].sum())
+        cpu = {"value": cdec / dt, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"first {sample} of {T} traces of the same workload, oracle/semsched_oracle.c "
+                         f"(C restatement of the reference scheduler), {threads} threads, {dt:.2f} s wall"}
+        match = bool(np.array_equal(res.stats["digest"], stats["digest"][:sample]) and
+                     np.array_equal(res.stats["rounds"], stats["rounds"][:sample]))
+        parity = {"traces_checked": sample, "digest_and_rounds_match": match}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl["desc"], "traces_per_gpu": T, "requests_per_trace": wl["requests"],
+                       "batch_size": 16, "memory_capacity": wl["capacity"], "profile": wl["profile"],
+                       "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"traces sharded x{world}",
+                       "kernel": {"blocks": cfgk["blocks"], "warps_per_block": cfgk["warps_per_block"],
+                                  "smem_per_block": cfgk["smem_per_block"]}},
+            "traces_per_s": traces_s,
+            "decisions_per_step": int(dec_t.item()) // args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": peak_src, "kernel_ms": k_ms,
+                         "algorithmic_bytes_per_launch": alg,
+                         "model": "SURVEY.md §8(d) B_decision summed over this launch's rounds"},
+            "cpu_baseline": cpu,
+            "parity": parity,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": args.steps * (1 + 0),
+            "failed_traces": bad,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

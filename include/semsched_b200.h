@@ -130,6 +130,11 @@ typedef struct ss_trace_stats {
                                   (the reference then carries a stale key and
                                   duplicate batch members; emulated) */
     int32_t  _pad;
+    /* per-round tallies for the algorithmic byte model         */
+    int64_t  sum_pool;         /* sum over rounds of live requests (heap+buffer+ongoing) */
+    int64_t  sum_granted;      /* sum of granted batch members                     */
+    int64_t  sum_victims;      /* victims processed (recorded + lost decisions)    */
+    int64_t  sum_resident_evict; /* residents, summed over rounds that evict       */
     double   final_clock;      /* RUN_END time                                     */
     /* CPython-3.12 float sum() (Neumaier) over completed records in trace order  */
     double   sum_wait;         /* sum(finish - arrival)                            */

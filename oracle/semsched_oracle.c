@@ -248,6 +248,8 @@ typedef struct {
     int status;
     int last_granted;
     int64_t lost_evictions, anomalies;
+    int64_t sum_pool, sum_granted, sum_victims, sum_res_evict;
+    int evict_round;
     /* scratch */
     int* cand; int* merged; int* granted; int* pushed;
     odecision* dec; int ndec, dec_cap;
@@ -413,6 +415,10 @@ static int priority_based_eviction(osim* s, int ri, int64_t demand, const int* p
     int skipped_cap = s->evq.n + 1;
     int* skipped = (int*)malloc(sizeof(int) * skipped_cap);
     int nsk = 0, rc = 0;
+    if (demand + s->used > s->cap && !s->evict_round) {
+        s->evict_round = 1;
+        s->sum_res_evict += s->evq.n;
+    }
     while (demand + s->used > s->cap) {
         int victim = -1;
         while (s->evq.n > 0) {
@@ -425,6 +431,7 @@ static int priority_based_eviction(osim* s, int ri, int64_t demand, const int* p
         if (victim < 0) { rc = -1; break; }
         if (h_contains(&s->heap, victim)) h_remove_at(&s->heap, s->r[victim].hpos);
         s->used -= s->r[victim].kv_dev;                          /* mem.release */
+        s->sum_victims++;
         push_dec(s, should_recompute(s, victim));
         heap_insert(s, victim);
     }
@@ -543,6 +550,7 @@ static void execute(osim* s, int kind, int m) {
     for (int q = 0; q < s->ndec; q++) s->evicted_flag[s->dec[q].victim] = 0;
 
     s->last_granted = ng;
+    s->sum_granted += ng;
     if (ng == 0) {                                                 /* :329-344 */
         s->nongoing = 0;
         s->eviction_count += s->ndec;
@@ -678,6 +686,8 @@ static void run_trace(const ss_params* P, const ss_trace_batch* B, const int64_t
         }
         int kind;
         int had_ongoing = s->nongoing;
+        s->sum_pool += live;
+        s->evict_round = 0;
         int m = schedule(s, &kind);
         if (m == 0) {
             if (next < npend) { s->clock = s->r[pending[next]].ready; continue; }
@@ -736,6 +746,10 @@ static void run_trace(const ss_params* P, const ss_trace_batch* B, const int64_t
     st.status = s->status;
     st.lost_evictions = (int32_t)s->lost_evictions;
     st.anomalies = (int32_t)s->anomalies;
+    st.sum_pool = s->sum_pool;
+    st.sum_granted = s->sum_granted;
+    st.sum_victims = s->sum_victims;
+    st.sum_resident_evict = s->sum_res_evict;
     st.final_clock = s->clock;
     st.sum_wait = pysum_value(&sw);
     st.sum_norm_wait = pysum_value(&sn);

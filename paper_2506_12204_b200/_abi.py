@@ -66,7 +66,9 @@ class ss_trace_stats(C.Structure):
     _fields_ = [("digest", C.c_uint64), ("rounds", C.c_int64), ("evictions", C.c_int64),
                 ("mem_used_peak", C.c_int64), ("log_words", C.c_int64),
                 ("completed", C.c_int32), ("unservable", C.c_int32), ("status", C.c_int32),
-                ("lost_evictions", C.c_int32), ("anomalies", C.c_int32), ("_pad", C.c_int32), ("final_clock", C.c_double), ("sum_wait", C.c_double),
+                ("lost_evictions", C.c_int32), ("anomalies", C.c_int32), ("_pad", C.c_int32),
+                ("sum_pool", C.c_int64), ("sum_granted", C.c_int64), ("sum_victims", C.c_int64),
+                ("sum_resident_evict", C.c_int64), ("final_clock", C.c_double), ("sum_wait", C.c_double),
                 ("sum_norm_wait", C.c_double), ("level_norm_sum", C.c_double * SS_MAX_LEVELS),
                 ("level_count", C.c_int32 * SS_MAX_LEVELS)]
 
@@ -95,7 +97,9 @@ def stats_dtype():
         STATS_DTYPE = np.dtype([
             ("digest", "<u8"), ("rounds", "<i8"), ("evictions", "<i8"), ("mem_used_peak", "<i8"),
             ("log_words", "<i8"), ("completed", "<i4"), ("unservable", "<i4"), ("status", "<i4"),
-            ("lost_evictions", "<i4"), ("anomalies", "<i4"), ("_pad", "<i4"), ("final_clock", "<f8"), ("sum_wait", "<f8"), ("sum_norm_wait", "<f8"),
+            ("lost_evictions", "<i4"), ("anomalies", "<i4"), ("_pad", "<i4"),
+            ("sum_pool", "<i8"), ("sum_granted", "<i8"), ("sum_victims", "<i8"), ("sum_resident_evict", "<i8"),
+            ("final_clock", "<f8"), ("sum_wait", "<f8"), ("sum_norm_wait", "<f8"),
             ("level_norm_sum", "<f8", (SS_MAX_LEVELS,)), ("level_count", "<i4", (SS_MAX_LEVELS,)),
         ])
         assert STATS_DTYPE.itemsize == C.sizeof(ss_trace_stats)

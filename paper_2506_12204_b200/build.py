@@ -16,8 +16,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libsemsched_b200.so")
-SOURCES = ["ss_kernel.cu", "ss_api.cu"]
-HEADERS = ["ss_kernel.cuh", "ss_costs.cuh", "../../include/semsched_b200.h"]
+SOURCES = ["ss_kernel.cu", "ss_api.cu", "ss_tracegen.cpp"]
+HEADERS = ["ss_kernel.cuh", "ss_costs.cuh", "../../include/semsched_b200.h",
+           "../../include/semsched_tracegen.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr"]
@@ -44,8 +45,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     objs = []
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
-        cmd = [nvcc()] + NVCC_FLAGS + ["-Xptxas", "-v"] * verbose + ["-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + ".o")
+        if src.endswith(".cpp"):
+            cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread",
+                   "-c", os.path.join(CSRC, src), "-o", obj]
+        else:
+            cmd = [nvcc()] + NVCC_FLAGS + ["-Xptxas", "-v"] * verbose + ["-c", os.path.join(CSRC, src), "-o", obj]
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"

@@ -143,6 +143,7 @@ struct Trace {
     int nF, nB, nR, nO, nins;
     long long rounds, evictions, peak;
     int status, nuns, lost, anomalies;
+    long long s_pool, s_granted, s_victims, s_res;
     long long logpos, logcap;
     uint32_t* log;
 };
@@ -493,6 +494,7 @@ __device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int 
     }
     if (ins_idx < 0) T.nins += 1;
     T.nR -= 1;
+    T.s_victims += 1;
     R.ndec += 1;
     __syncwarp();
     // every batch copy of the victim is skipped (evicted_ids is by id) and refreshed
@@ -553,6 +555,7 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
         T.status = SS_TRACE_OK;
         T.nuns = 0;
         T.lost = T.anomalies = 0;
+        T.s_pool = T.s_granted = T.s_victims = T.s_res = 0;
         T.logpos = 0;
         T.log = nullptr;
         T.logcap = 0;
@@ -629,6 +632,7 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 continue;
             }
             if (T.nF < b && T.nB > 0) refill(E, T);
+            T.s_pool += live;
 
             // ---- stage-aware composition (batching.py:46-88)
             const int nc = T.nF < b ? T.nF : b;
@@ -792,6 +796,7 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                     }
                 }
                 if (nm) {
+                    T.s_res += T.nR;
                     // slow path: one member at a time from the first that must evict
                     long long reserved = __shfl_sync(FULL, excl, f);
                     if ((R.G >> lane) & 1u) {
@@ -885,6 +890,7 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
             T.evictions += R.ndec;
             const bool g_act = (R.G >> lane) & 1u;
             const int ng = __popc(R.G);
+            T.s_granted += ng;
             const unsigned long long r64 = (unsigned long long)T.rounds;
 
             if (ng == 0) {
@@ -1229,6 +1235,10 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 st->lost_evictions = T.lost;
                 st->anomalies = T.anomalies;
                 st->_pad = 0;
+                st->sum_pool = T.s_pool;
+                st->sum_granted = T.s_granted;
+                st->sum_victims = T.s_victims;
+                st->sum_resident_evict = T.s_res;
                 st->final_clock = T.clock;
             }
         }

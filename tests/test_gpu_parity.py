@@ -69,7 +69,8 @@ def _compare_with_oracle(gpu, cpu, batch):
     assert np.array_equal(gpu.stats["status"], cpu.stats["status"]), "status"
     ok = cpu.stats["status"] == 0
     for k in ("rounds", "evictions", "digest", "completed", "unservable", "mem_used_peak",
-              "lost_evictions", "anomalies"):
+              "lost_evictions", "anomalies", "sum_pool", "sum_granted", "sum_victims",
+              "sum_resident_evict"):
         assert np.array_equal(gpu.stats[k][ok], cpu.stats[k][ok]), k
     for k in ("final_clock", "sum_wait", "sum_norm_wait", "level_norm_sum"):
         assert np.array_equal(gpu.stats[k][ok].view(np.uint64), cpu.stats[k][ok].view(np.uint64)), k
