@@ -105,14 +105,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def build_batch(wl, rank, traces_override=None):
+def build_batch(wl, rank, traces_override=None, pinned=True):
     from paper_2506_12204_b200.tracegen import generate_batch
     from paper_2506_12204_b200.workload import WorkloadSpec
 
     T = traces_override or wl["traces"]
     seeds = np.arange(rank * T, (rank + 1) * T, dtype=np.int64)
     spec = WorkloadSpec(total_requests=wl["requests"], levels=wl["levels"])
-    return generate_batch(spec, seeds, pinned=True), T
+    return generate_batch(spec, seeds, pinned=pinned), T
 
 
 def algorithmic_bytes(stats, n_req):
@@ -141,8 +141,6 @@ def cpu_oracle(params_fn, batch, sample, threads):
 
 def reference_arm(args, wl):
     """The reference's CPU scheduler, timed on this box's host cores."""
-    import torch  # noqa: F401  (pinned buffers in generate_batch)
-
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -150,7 +148,7 @@ def reference_arm(args, wl):
     from paper_2506_12204_b200.results import make_params
     from paper_2506_12204_b200 import _abi as A
 
-    batch, T = build_batch(wl, 0, args.traces)
+    batch, T = build_batch(wl, 0, args.traces, pinned=False)
     threads = os.cpu_count() or 1
     sample = min(T, max(threads * 2, 64))
     pf = lambda: make_params(get_profile(wl["profile"]), 16, wl["capacity"], levels=wl["levels"], flags=A.SS_FLAG_DIGEST)
