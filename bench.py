@@ -278,7 +278,7 @@ def main():
 
         hb = native.host_batch(batch)
         outs = alloc_host_outputs(n_req, T)
-        pin = lambda a: torch.from_numpy(a).pin_memory().numpy() if a.size else a
+        pin = lambda a: torch.from_numpy(a.view(np.uint8)).pin_memory().numpy().view(a.dtype) if a.size else a
         outs = {k: pin(v) for k, v in outs.items()}
         o = A.ss_outputs()
         o.req = A.ss_request_out(outs["first_scheduled"].ctypes.data, outs["finish_time"].ctypes.data,

@@ -200,7 +200,7 @@ SS_HD uint64_t ss_mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 SS_HD uint64_t ss_term(uint64_t round, uint32_t tag, uint32_t idx, uint64_t v) {
-    return ss_mix64(ss_mix64((round << 24) ^ ((uint64_t)tag << 20) ^ (uint64_t)idx) ^ v);
+    return ss_mix64(v ^ (((round << 24) ^ ((uint64_t)tag << 20) ^ (uint64_t)idx) * 0x9E3779B97F4A7C15ull));
 }
 #define SS_TAG_HDR   1u
 #define SS_TAG_MEM   2u

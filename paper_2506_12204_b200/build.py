@@ -39,8 +39,10 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """``defines``/``out`` build an experimental variant (e.g. SS_MINB=6)."""
+    lib = out or LIB
+    if not force and not _stale() and out is None:
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     objs = []
@@ -50,16 +52,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread",
                    "-c", os.path.join(CSRC, src), "-o", obj]
         else:
-            cmd = [nvcc()] + NVCC_FLAGS + ["-Xptxas", "-v"] * verbose + ["-c", os.path.join(CSRC, src), "-o", obj]
+            cmd = ([nvcc()] + NVCC_FLAGS + ["-Xptxas", "-v"] * verbose + [f"-D{d}" for d in defines]
+                   + ["-c", os.path.join(CSRC, src), "-o", obj])
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.run([nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv or bool(defs), verbose="-v" in sys.argv, defines=defs,
+                out=outs[0] if outs else None))

@@ -31,6 +31,10 @@
 #include "ss_costs.cuh"
 #include "ss_kernel.cuh"
 
+#ifndef SS_MINB
+#define SS_MINB 1  // min resident CTAs per SM requested from ptxas (register cap)
+#endif
+
 namespace ss {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -71,6 +75,13 @@ __device__ __forceinline__ Key kshfl(const Key& k, int src) {
     r.hi = __shfl_sync(FULL, k.hi, src);
     r.lo = __shfl_sync(FULL, k.lo, src);
     r.aux = __shfl_sync(FULL, k.aux, src);
+    return r;
+}
+__device__ __forceinline__ Key kshfl_down(const Key& k, int d) {
+    Key r;
+    r.hi = __shfl_down_sync(FULL, k.hi, d);
+    r.lo = __shfl_down_sync(FULL, k.lo, d);
+    r.aux = __shfl_down_sync(FULL, k.aux, d);
     return r;
 }
 __device__ __forceinline__ Key kshfl_xor(const Key& k, int m) {
@@ -527,7 +538,7 @@ __device__ __forceinline__ MemQ mem_q(const MemS& m) {
 // the kernel
 // --------------------------------------------------------------------------
 template <int POL>
-__global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
+__global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs args) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const KArgs& A = args;
     const int lane = threadIdx.x & 31;
@@ -645,15 +656,21 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 load_mem(A, T.off, ck.aux & SLOT_MASK, cm);  // used if selected
                 if (anom) ck = make_key<POL>(cm.urank, cm.ft, cm.tie, cm.slot, (cm.flg & F_STAGE) == ST_DEC);
             }
-            // p* = min over candidates and ongoing (current keys)
-            Key pmin = has_o ? okey : kinf();
-            if (anom || lane == 0) {
+            // p* = min over candidates and ongoing (current keys). The ongoing
+            // copies are kept sorted by key across lanes (order among them is
+            // unobservable in the reference: equal keys are the same request).
+            Key pmin = kinf();
+            if (!anom) {
+                if (T.nO > 0) pmin = kshfl(okey, 0);
+                if (nc > 0 && klt(sm->F[0], pmin)) pmin = sm->F[0];
+            } else {
+                pmin = has_o ? okey : kinf();
                 if (has_c && klt(ck, pmin)) pmin = ck;
-            }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                Key x = kshfl_xor(pmin, o);
-                if (klt(x, pmin)) pmin = x;
+                for (int o = 16; o > 0; o >>= 1) {
+                    Key x = kshfl_xor(pmin, o);
+                    if (klt(x, pmin)) pmin = x;
+                }
             }
             const bool pstar_prefill = !(pmin.aux & DEC_BIT);
             const int kind = pstar_prefill ? SS_KIND_PREFILL : SS_KIND_DECODE;
@@ -661,25 +678,31 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
             const unsigned cmask = __ballot_sync(FULL, c_elig);
             int cnt_c = 0, cnt_o = 0;
             if (!anom) {
-                // candidates are FRONT[0..nc), already sorted: merge by rank
-                if (has_o) sm->X[32 + lane] = okey;
-                __syncwarp();
-                for (int k = 0; k < T.nO; k++) {
-                    Key x = sm->X[32 + k];
-                    if (c_elig && klt(x, ck)) cnt_c++;
-                    if (has_o && klt(x, okey)) cnt_o++;
-                }
-                if (has_o) {
-                    int lo = 0, hi = nc;
-                    while (lo < hi) {
-                        int mid = (lo + hi) >> 1;
-                        if (klt(sm->F[mid], okey)) lo = mid + 1;
-                        else hi = mid;
+                // both lists sorted: ranks are own index + lower_bound in the other
+                cnt_o = lane;
+                if (cmask) {
+                    if (has_o) sm->X[32 + lane] = okey;
+                    __syncwarp();
+                    if (c_elig) {
+                        int lo = 0, hi = T.nO;
+                        while (lo < hi) {
+                            int mid = (lo + hi) >> 1;
+                            if (klt(sm->X[32 + mid], ck)) lo = mid + 1;
+                            else hi = mid;
+                        }
+                        cnt_c = __popc(cmask & lt) + lo;
                     }
-                    unsigned below = lo >= 32 ? FULL : ((1u << lo) - 1u);
-                    cnt_o += __popc(cmask & below);
+                    if (has_o) {
+                        int lo = 0, hi = nc;
+                        while (lo < hi) {
+                            int mid = (lo + hi) >> 1;
+                            if (klt(sm->F[mid], okey)) lo = mid + 1;
+                            else hi = mid;
+                        }
+                        unsigned below = lo >= 32 ? FULL : ((1u << lo) - 1u);
+                        cnt_o += __popc(cmask & below);
+                    }
                 }
-                cnt_c += __popc(cmask & lt);
             } else {
                 // general: stable sort of (candidates + ongoing) by current key;
                 // equal keys are copies of one request, ordered by pool position
@@ -777,8 +800,19 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
             // ---- admission with KV budget (engine.py:296-327)
             MemQ q = mem_q(mem);
             {
-                long long inc = act ? q.imm : 0;
-                long long excl = warp_incl_scan_ll(inc, lane) - inc;
+                long long excl;
+                if (__all_sync(FULL, !act || q.isdec)) {
+                    excl = lane;  // every immediate is 1
+                } else {
+                    int inc = act ? (int)q.imm : 0;
+                    int sc = inc;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        int tt = __shfl_up_sync(FULL, sc, o);
+                        if (lane >= o) sc += tt;
+                    }
+                    excl = (long long)(sc - inc);
+                }
                 long long dem = q.est > q.imm ? q.est : q.imm;
                 if (dem + excl > T.cap) dem = q.imm;
                 bool need = act && (dem + excl + T.used > T.cap);
@@ -938,15 +972,16 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 }
                 const unsigned dm = __ballot_sync(FULL, g_act && q.isdec);
                 if (dm) {
-                    double st = (g_act && q.isdec)
-                                    ? decode_step_time((long long)mem.prompt + mem.dec + 1, 1, P)
-                                    : -INFINITY;
                     double part;
                     if (!A.P.decode_cost_sum) {
-                        part = st;
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) part = fmax(part, __shfl_xor_sync(FULL, part, o));
+                        // gamma1 >= 0: the step time is monotone in the context length,
+                        // so the max step is the step of the longest context
+                        unsigned nmax = __reduce_max_sync(FULL, (g_act && q.isdec) ? mem.prompt + mem.dec + 1u : 0u);
+                        part = decode_step_time((long long)nmax, 1, P);
                     } else {
+                        double st = (g_act && q.isdec)
+                                        ? decode_step_time((long long)mem.prompt + mem.dec + 1, 1, P)
+                                        : 0.0;
                         PySum ps;
                         ps.init();
                         for (int k = 0; k < m; k++) {
@@ -995,7 +1030,7 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                         A.w.flg[g] = mem.flg;
                     }
                     // allocations all fit (admission reserved them); completions release
-                    T.used += warp_sum_ll(delta);
+                    T.used += (long long)__reduce_add_sync(FULL, (int)delta);
                     if (T.used > T.cap || T.used < 0) set_status(T, SS_TRACE_INTERNAL);
                     const unsigned nm = __ballot_sync(FULL, newres);
                     if (newres) {
@@ -1110,11 +1145,9 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 if (A.P.flags & SS_FLAG_DIGEST) {
                     if (g_act) dig += ss_term(r64, SS_TAG_GRANT, gi, mem.slot);
                     if (done) dig += ss_term(r64, SS_TAG_DONE, ci, mem.slot);
-                    if (lane == 0) {
-                        dig += ss_term(r64, SS_TAG_HDR, 0, ss_hdr_word(kind, ng, nc_done, R.ndec));
-                        dig += ss_term(r64, SS_TAG_MEM, 0, (unsigned long long)T.used);
-                        dig += ss_term(r64, SS_TAG_TIME, 0, dbits(end));
-                    }
+                    if (lane == 31) dig += ss_term(r64, SS_TAG_HDR, 0, ss_hdr_word(kind, ng, nc_done, R.ndec));
+                    if (lane == 30) dig += ss_term(r64, SS_TAG_MEM, 0, (unsigned long long)T.used);
+                    if (lane == 29) dig += ss_term(r64, SS_TAG_TIME, 0, dbits(end));
                 }
                 if (T.log) {
                     long long base = T.logpos + SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * R.ndec;
@@ -1146,6 +1179,26 @@ __global__ void __launch_bounds__(32 * WPB) sched_kernel(const KArgs args) {
                 if (lane < T.nO) {
                     om = sm->M[lane];
                     okey = make_key<POL>(om.urank, om.ft, om.tie, om.slot, true);
+                }
+                // keep the ongoing copies sorted by their new keys (usually they are)
+                {
+                    Key nk = kshfl_down(okey, 1);
+                    if (__ballot_sync(FULL, lane + 1 < T.nO && klt(nk, okey))) {
+                        if (lane < T.nO) sm->X[32 + lane] = okey;
+                        __syncwarp();
+                        int r = 0;
+                        for (int k = 0; k < T.nO; k++) {
+                            Key x = sm->X[32 + k];
+                            if (klt(x, okey) || (keq(x, okey) && k < lane)) r++;
+                        }
+                        __syncwarp();
+                        if (lane < T.nO) sm->M[r] = om;
+                        __syncwarp();
+                        if (lane < T.nO) {
+                            om = sm->M[lane];
+                            okey = make_key<POL>(om.urank, om.ft, om.tie, om.slot, true);
+                        }
+                    }
                 }
             }
             if (T.log && T.logpos > T.logcap) set_status(T, SS_TRACE_LOG_OVERFLOW);

@@ -17,7 +17,8 @@ import numpy as np
 from . import _abi as A
 from .results import RunResult, alloc_host_outputs, collect, log_capacity_words
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsemsched_b200.so")
+LIB_PATH = os.environ.get("SS_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                         "libsemsched_b200.so")
 _lib = None
 
 

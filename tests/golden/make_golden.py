@@ -53,7 +53,8 @@ def mix64(z):
 
 
 def term(rnd, tag, idx, v):
-    return mix64(mix64(((rnd << 24) ^ (tag << 20) ^ idx) & M64) ^ (v & M64))
+    salt = ((((rnd << 24) ^ (tag << 20) ^ idx) & M64) * 0x9E3779B97F4A7C15) & M64
+    return mix64((v & M64) ^ salt)
 
 
 def fbits(x):

@@ -22,8 +22,8 @@ _lib = None
 
 
 def build_oracle() -> str:
-    src = os.path.join(ORACLE_DIR, "semsched_oracle.c")
-    if not os.path.exists(ORACLE_SO) or os.path.getmtime(ORACLE_SO) < os.path.getmtime(src):
+    deps = [os.path.join(ORACLE_DIR, "semsched_oracle.c"), os.path.join(REPO, "include", "semsched_b200.h")]
+    if not os.path.exists(ORACLE_SO) or os.path.getmtime(ORACLE_SO) < max(os.path.getmtime(d) for d in deps):
         subprocess.run(["make", "-s", "-C", ORACLE_DIR], check=True)
     return ORACLE_SO
 
