@@ -3,7 +3,7 @@
 // One warp owns one arrival trace and runs every scheduler round of it
 // (the reference's Simulator.run loop, engine.py:202-224) without leaving the
 // SM. Traces are independent, so warps pull trace ids from a global counter
-// (persistent, load-balanced); 4,096 traces keep ~28 warps resident per SM.
+// (persistent, load-balanced).
 //
 // Per-trace state:
 //   * dispatch queue = sorted FRONT (64 packed keys, shared memory) + unsorted
@@ -11,10 +11,12 @@
 //     top-b candidates are FRONT[0..b) and the dual heap of heaps.py:32-237
 //     becomes a merge-by-rank in shared memory. The BACK is refilled with a
 //     warp bitonic top-32 selection when the FRONT runs short.
-//   * ongoing batch (engine.py:165) lives in registers: lane i = member i.
+//   * ongoing batch (engine.py:165): one record per lane, kept sorted by key,
+//     stored in shared memory between rounds (keys stay in registers).
 //   * resident set (the eviction heap, heaps.py:174-207) is an unsorted HBM
 //     list scanned with a warp arg-max only when memory is short.
-//   * per-request dynamic state (f_t, decoded, stage bits) is SoA in HBM.
+//   * per-request state is two 16-byte HBM records: static (prompt, true
+//     output, predicted length, rank|tie) and dynamic (f_t, decoded, flags).
 //
 // Packed dispatch key (requests.py:81-91, engine.py:114-123), 96 bits:
 //   hi = rank:8 | f_t bits 62..7        lo = f_t bits 6..0 | tie:25
@@ -31,6 +33,11 @@
 #include "ss_costs.cuh"
 #include "ss_kernel.cuh"
 
+#ifdef SS_EVICT_NOINLINE
+#define SS_EVICT_INLINE __device__ __noinline__
+#else
+#define SS_EVICT_INLINE __device__ __forceinline__
+#endif
 #ifndef SS_MINB
 #define SS_MINB 1  // min resident CTAs per SM requested from ptxas (register cap)
 #endif
@@ -48,21 +55,47 @@ struct __align__(16) Key {
     uint32_t aux;  // slot | decoding << 31
 };
 
+// a request's state as one unit: static record, dynamic record, slot
 struct __align__(16) MemS {
+    uint4 st;      // prompt, true_out, pred_len, rank << 24 | tie
+    double ft;     // \ dynamic record (Dyn)
+    uint32_t dec;  //  |
+    uint32_t flg;  // /
+    uint32_t slot, _pad0, _pad1, _pad2;
+};
+
+// dynamic record of a request in HBM
+struct __align__(16) Dyn {
     double ft;
-    uint32_t slot, prompt, tout, mid;
-    uint32_t urank, tie, dec, flg;
+    uint32_t dec;
+    uint32_t flg;
+};
+
+// trace state touched once per round or less: shared memory, lane 0 writes
+struct Cold {
+    long long evictions, peak, s_pool, s_granted, s_victims, s_res, logpos, logcap;
+    uint32_t* log;
+    int nuns, lost, anomalies, n;
 };
 
 struct WarpSmem {
     Key F[FCAP];    // sorted queue front
     Key X[64];      // scratch keys (pool ranking: candidates 0..31, ongoing 32..63)
     MemS M[32];     // member hand-off between lanes
+    MemS OM[32];    // ongoing records, lane order = key order
+    Cold c;
 };
+
+__device__ __forceinline__ uint32_t m_prompt(const MemS& m) { return m.st.x; }
+__device__ __forceinline__ uint32_t m_tout(const MemS& m) { return m.st.y; }
+__device__ __forceinline__ uint32_t m_mid(const MemS& m) { return m.st.z; }
+__device__ __forceinline__ uint32_t m_rank(const MemS& m) { return m.st.w >> 24; }
+__device__ __forceinline__ uint32_t m_tie(const MemS& m) { return m.st.w & SLOT_MASK; }
 
 __device__ __forceinline__ bool klt(const Key& a, const Key& b) {
     return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo);
 }
+__device__ __forceinline__ bool keq(const Key& a, const Key& b) { return a.hi == b.hi && a.lo == b.lo; }
 __device__ __forceinline__ Key kinf() {
     Key k;
     k.hi = ~0ull;
@@ -96,22 +129,9 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
     return r;
 }
-__device__ __forceinline__ long long warp_sum_ll(long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
-}
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
-}
-__device__ __forceinline__ long long warp_incl_scan_ll(long long v, int lane) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        long long t = __shfl_up_sync(FULL, v, o);
-        if (lane >= o) v += t;
-    }
     return v;
 }
 
@@ -136,27 +156,31 @@ __device__ __forceinline__ Key make_key(uint32_t urank, double ft, uint32_t tie,
     k.aux = slot | (decoding ? DEC_BIT : 0u);
     return k;
 }
+template <int POL>
+__device__ __forceinline__ Key mem_key(const MemS& m) {
+    return make_key<POL>(m_rank(m), m.ft, m_tie(m), m.slot, (m.flg & F_STAGE) == ST_DEC);
+}
 
 __device__ __forceinline__ Key* BK(const KArgs& A) { return reinterpret_cast<Key*>(A.w.B); }
+__device__ __forceinline__ Key* INS(const KArgs& A) { return reinterpret_cast<Key*>(A.w.ins); }
+__device__ __forceinline__ uint4* STA(const KArgs& A) { return reinterpret_cast<uint4*>(A.w.st); }
+__device__ __forceinline__ Dyn* DYN(const KArgs& A) { return reinterpret_cast<Dyn*>(A.w.dy); }
 
 __device__ __forceinline__ unsigned long long dbits(double x) {
     return (unsigned long long)__double_as_longlong(x);
 }
 
 // --------------------------------------------------------------------------
-// trace context (warp-uniform)
+// trace context: hot, warp-uniform values in registers
 // --------------------------------------------------------------------------
 struct Trace {
     long long off;
-    int n, npend, cursor;
+    long long used;
     double clock;
-    long long used, cap;
+    double next_ready;  // ready time of the next pending request (inf if none)
+    int npend, cursor;
     int nF, nB, nR, nO, nins;
-    long long rounds, evictions, peak;
-    int status, nuns, lost, anomalies;
-    long long s_pool, s_granted, s_victims, s_res;
-    long long logpos, logcap;
-    uint32_t* log;
+    int rounds, status;
 };
 
 struct Env {
@@ -166,17 +190,22 @@ struct Env {
 };
 
 __device__ __forceinline__ void load_mem(const KArgs& A, long long off, uint32_t slot, MemS& m) {
-    long long g = off + slot;
+    const long long g = off + slot;
+    m.st = STA(A)[g];
+    const Dyn d = DYN(A)[g];
+    m.ft = d.ft;
+    m.dec = d.dec;
+    m.flg = d.flg;
     m.slot = slot;
-    m.prompt = __ldg(A.in.prompt_len + g);
-    m.tout = __ldg(A.in.true_output_len + g);
-    m.mid = __ldg(A.in.pred_len + g);
-    m.urank = __ldg(A.in.pred_urgency + g);
-    m.tie = __ldg(A.in.tie_rank + g);
-    m.dec = A.w.dec[g];
-    m.flg = A.w.flg[g];
-    m.ft = A.w.ft[g];
 }
+__device__ __forceinline__ void store_dyn(const KArgs& A, long long g, double ft, uint32_t dec, uint32_t flg) {
+    Dyn d;
+    d.ft = ft;
+    d.dec = dec;
+    d.flg = flg;
+    DYN(A)[g] = d;
+}
+__device__ __forceinline__ uint32_t* FLG(const KArgs& A, long long g) { return &DYN(A)[g].flg; }
 
 // ---- queue front / back maintenance --------------------------------------
 
@@ -332,13 +361,10 @@ __device__ void refill(const Env& E, Trace& T) {
     T.nB = w;
 }
 
-// ---- logging / digest -----------------------------------------------------
-__device__ __forceinline__ void log_put(Trace& T, long long pos, uint32_t v) {
-    if (T.log && pos < T.logcap) T.log[pos] = v;
+// ---- logging ---------------------------------------------------------------
+__device__ __forceinline__ void log_put(const Cold& c, long long pos, uint32_t v) {
+    if (c.log && pos < c.logcap) c.log[pos] = v;
 }
-
-__device__ __forceinline__ Key* INS(const KArgs& A) { return reinterpret_cast<Key*>(A.w.ins); }
-__device__ __forceinline__ bool keq(const Key& a, const Key& b) { return a.hi == b.hi && a.lo == b.lo; }
 
 struct Round {
     unsigned G;                // granted batch positions
@@ -400,12 +426,13 @@ __device__ void q_delete(const Env& E, Trace& T, Round& R, uint32_t v, uint32_t 
 
 // Evict one victim for member `kslot` (kvcache.py:160-175): the resident with
 // the largest dispatch key that is neither granted this round nor `kslot`.
-// Returns false if there is none (AdmissionFailure).
+// Returns false if there is none (AdmissionFailure). Cold path: not inlined.
 template <int POL>
-__device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int m, MemS& mem,
-                          unsigned& vcall) {
+SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int m, MemS& mem,
+                                       unsigned& vcall) {
     const KArgs& A = *E.A;
     const int lane = E.lane;
+    Cold& c = E.sm->c;
     const ss_profile& P = A.P.profile;
     Key best;
     bool have = false;
@@ -415,9 +442,10 @@ __device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int 
         if (i < T.nR) {
             uint32_t s = A.w.R[T.off + i];
             long long g = T.off + s;
-            uint32_t f = A.w.flg[g];
-            if (!(f & F_GRANT) && s != kslot) {
-                Key k = make_key<POL>(__ldg(A.in.pred_urgency + g), A.w.ft[g], __ldg(A.in.tie_rank + g), s, true);
+            const Dyn d = DYN(A)[g];
+            if (!(d.flg & F_GRANT) && s != kslot) {
+                const uint32_t w = STA(A)[g].w;
+                Key k = make_key<POL>(w >> 24, d.ft, w & SLOT_MASK, s, true);
                 if (!have || klt(best, k)) {
                     best = k;
                     have = true;
@@ -442,10 +470,11 @@ __device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int 
     const uint32_t v = best.aux & SLOT_MASK;
     const long long gv = T.off + v;
     // ---- should_recompute (kvcache.py:81-134), evaluated redundantly per lane
-    uint32_t prompt = __ldg(A.in.prompt_len + gv), mid = __ldg(A.in.pred_len + gv);
-    uint32_t dec = A.w.dec[gv], flg = A.w.flg[gv];
-    double ftb = A.w.ft[gv];
-    long long freed = (long long)prompt + dec;
+    MemS vm;
+    load_mem(A, T.off, v, vm);
+    const uint32_t prompt = m_prompt(vm), dec = vm.dec, flg = vm.flg;
+    const double ftb = vm.ft;
+    const long long freed = (long long)prompt + dec;
     bool pf = (flg & F_PF) != 0;
     int action;
     long long psaved;
@@ -459,39 +488,36 @@ __device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int 
     }
     long long saved = dec > 0 ? optimal_save_tokens(prompt, dec, P) : 0;
     if (action == 1 && A.P.dependency_rule) saved = 0;
-    long long discarded = (long long)dec - saved;
-    long long kvh = psaved + saved;
-    double fta = remaining_time(prompt, mid, pf ? prompt : 0, saved, kvh, P);
+    const long long discarded = (long long)dec - saved;
+    const double fta = remaining_time(prompt, m_mid(vm), pf ? prompt : 0, saved, psaved + saved, P);
     T.used -= freed;
-    const Key nkey = make_key<POL>(__ldg(A.in.pred_urgency + gv), fta, __ldg(A.in.tie_rank + gv), v, false);
+    const Key nkey = make_key<POL>(m_rank(vm), fta, m_tie(vm), v, false);
     // heap: delete_by_id if queued, then insert with the new key
     int ins_idx = -1;
     if ((flg & F_Q) && (flg & F_INS)) ins_idx = ins_find(A, T, v, lane);
     else q_delete(E, T, R, v, flg);
-    uint32_t nflg = (flg & ~(F_STAGE | F_PF)) | ST_WAIT | (pf ? F_PF : 0u) | F_Q | F_INS;
+    const uint32_t nflg = (flg & ~(F_STAGE | F_PF)) | ST_WAIT | (pf ? F_PF : 0u) | F_Q | F_INS;
     if (lane == 0) {
         uint32_t last = A.w.R[T.off + T.nR - 1];  // resident list: swap-remove
         A.w.R[T.off + best_ri] = last;
         A.w.rpos[T.off + last] = (uint32_t)best_ri;
         if (ins_idx >= 0) INS(A)[T.off + ins_idx] = nkey;
         else INS(A)[T.off + T.nins] = nkey;
-        A.w.flg[gv] = nflg;
-        A.w.dec[gv] = (uint32_t)saved;
-        A.w.ft[gv] = fta;
+        store_dyn(A, gv, fta, (uint32_t)saved, nflg);
         A.out.req.evictions[gv] += 1u;
-        int d = R.ndec;  // decision record: kept only if the admission succeeds
-        if (T.log) {
-            long long p = T.logpos + SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * d;
+        const int d = R.ndec;  // decision record: kept only if the admission succeeds
+        if (c.log) {
+            long long p = c.logpos + SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * d;
             unsigned long long fb = dbits(ftb), fa = dbits(fta);
-            log_put(T, p + 0, v);
-            log_put(T, p + 1, (uint32_t)action);
-            log_put(T, p + 2, (uint32_t)saved);
-            log_put(T, p + 3, (uint32_t)discarded);
-            log_put(T, p + 4, (uint32_t)freed);
-            log_put(T, p + 5, (uint32_t)fb);
-            log_put(T, p + 6, (uint32_t)(fb >> 32));
-            log_put(T, p + 7, (uint32_t)fa);
-            log_put(T, p + 8, (uint32_t)(fa >> 32));
+            log_put(c, p + 0, v);
+            log_put(c, p + 1, (uint32_t)action);
+            log_put(c, p + 2, (uint32_t)saved);
+            log_put(c, p + 3, (uint32_t)discarded);
+            log_put(c, p + 4, (uint32_t)freed);
+            log_put(c, p + 5, (uint32_t)fb);
+            log_put(c, p + 6, (uint32_t)(fb >> 32));
+            log_put(c, p + 7, (uint32_t)fa);
+            log_put(c, p + 8, (uint32_t)(fa >> 32));
         }
         if (A.P.flags & SS_FLAG_DIGEST) {
             unsigned long long r = (unsigned long long)T.rounds;
@@ -502,35 +528,34 @@ __device__ bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int 
             R.dpend += ss_term(r, SS_TAG_EV3, d, dbits(ftb));
             R.dpend += ss_term(r, SS_TAG_EV4, d, dbits(fta));
         }
+        c.s_victims += 1;
     }
     if (ins_idx < 0) T.nins += 1;
     T.nR -= 1;
-    T.s_victims += 1;
     R.ndec += 1;
     __syncwarp();
     // every batch copy of the victim is skipped (evicted_ids is by id) and refreshed
-    unsigned bpos = __ballot_sync(FULL, lane < m && mem.slot == v);
+    const unsigned bpos = __ballot_sync(FULL, lane < m && mem.slot == v);
     vcall |= bpos;
     if ((bpos >> lane) & 1u) load_mem(A, T.off, v, mem);
     __syncwarp();
     return true;
 }
 
-// ---- per-lane member quantities ------------------------------------------
+// ---- per-lane member quantities (32-bit: token counts of one request) -------
 struct MemQ {
-    bool isdec, pf;
-    long long pfn, kvh, kvd, imm, est;
+    bool isdec;
+    uint32_t pfn, kvh, kvd, imm, est;
 };
 __device__ __forceinline__ MemQ mem_q(const MemS& m) {
     MemQ q;
     q.isdec = (m.flg & F_STAGE) == ST_DEC;
-    q.pf = (m.flg & F_PF) != 0;
-    q.pfn = q.pf ? (long long)m.prompt : 0;
-    q.kvh = q.isdec ? 0 : q.pfn + m.dec;
-    q.kvd = q.isdec ? (long long)m.prompt + m.dec : 0;
-    q.imm = q.isdec ? 1 : q.kvh + ((long long)m.prompt - q.pfn) + 1;
-    long long e = (long long)m.prompt + m.mid - q.kvd;
-    q.est = e > 0 ? e : 0;
+    q.pfn = (m.flg & F_PF) ? m_prompt(m) : 0u;
+    q.kvh = q.isdec ? 0u : q.pfn + m.dec;
+    q.kvd = q.isdec ? m_prompt(m) + m.dec : 0u;
+    q.imm = q.isdec ? 1u : q.kvh + (m_prompt(m) - q.pfn) + 1u;
+    const long long e = (long long)m_prompt(m) + m_mid(m) - q.kvd;
+    q.est = e > 0 ? (uint32_t)e : 0u;
     return q;
 }
 
@@ -544,10 +569,14 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     WarpSmem* sm = reinterpret_cast<WarpSmem*>(smem_raw) + wib;
+    Cold& c = sm->c;
     Env E{&A, sm, lane};
     const ss_profile& P = A.P.profile;
     const int b = A.P.batch_size;
+    const long long cap = A.P.memory_capacity;
     const unsigned lt = lanemask_lt();
+    const bool want_digest = (A.P.flags & SS_FLAG_DIGEST) != 0;
+    const bool logging = (A.P.flags & SS_FLAG_ROUND_LOG) && A.out.round_log && A.out.log_offsets;
 
     for (;;) {
         int t = 0;
@@ -557,61 +586,67 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
 
         Trace T;
         T.off = A.in.trace_offsets[t];
-        T.n = (int)(A.in.trace_offsets[t + 1] - T.off);
-        T.cap = A.P.memory_capacity;
+        const int n = (int)(A.in.trace_offsets[t + 1] - T.off);
         T.clock = 0.0;
         T.used = 0;
         T.nF = T.nB = T.nR = T.nO = T.nins = 0;
-        T.rounds = T.evictions = T.peak = 0;
+        T.rounds = 0;
         T.status = SS_TRACE_OK;
-        T.nuns = 0;
-        T.lost = T.anomalies = 0;
-        T.s_pool = T.s_granted = T.s_victims = T.s_res = 0;
-        T.logpos = 0;
-        T.log = nullptr;
-        T.logcap = 0;
         bool anom = false;  // a stale heap entry may exist: general (exact) round path
-        if ((A.P.flags & SS_FLAG_ROUND_LOG) && A.out.round_log && A.out.log_offsets) {
-            T.log = A.out.round_log + A.out.log_offsets[t];
-            T.logcap = A.out.log_offsets[t + 1] - A.out.log_offsets[t];
+        if (lane == 0) {
+            c.evictions = c.peak = c.s_pool = c.s_granted = c.s_victims = c.s_res = 0;
+            c.logpos = 0;
+            c.log = nullptr;
+            c.logcap = 0;
+            if ((A.P.flags & SS_FLAG_ROUND_LOG) && A.out.round_log && A.out.log_offsets) {
+                c.log = A.out.round_log + A.out.log_offsets[t];
+                c.logcap = A.out.log_offsets[t + 1] - A.out.log_offsets[t];
+            }
+            c.nuns = c.lost = c.anomalies = 0;
+            c.n = n;
         }
         unsigned long long dig = 0ull;
 
-        // ---- init (engine.py:183-199): f_t, unservable pre-filter, pending list
+        // ---- init (engine.py:183-199): records, f_t, pre-filter, pending list
         T.npend = 0;
-        for (int base = 0; base < T.n; base += 32) {
+        int nuns = 0;
+        for (int base = 0; base < n; base += 32) {
             int i = base + lane;
-            bool v = i < T.n;
+            bool v = i < n;
             bool serv = false;
             if (v) {
                 long long g = T.off + i;
-                uint32_t prompt = A.in.prompt_len[g], mid = A.in.pred_len[g];
-                A.w.ft[g] = remaining_time(prompt, mid, 0, 0, 0, P);
-                A.w.dec[g] = 0u;
+                const uint32_t prompt = A.in.prompt_len[g], mid = A.in.pred_len[g];
+                uint4 st;
+                st.x = prompt;
+                st.y = A.in.true_output_len[g];
+                st.z = mid;
+                st.w = ((uint32_t)A.in.pred_urgency[g] << 24) | A.in.tie_rank[g];
+                STA(A)[g] = st;
+                serv = (long long)prompt + 1 <= cap;
+                store_dyn(A, g, remaining_time(prompt, mid, 0, 0, 0, P), 0u, serv ? ST_WAIT : ST_UNS);
                 A.out.req.first_scheduled[g] = __longlong_as_double(0x7ff8000000000000ll);
                 A.out.req.finish_time[g] = __longlong_as_double(0x7ff8000000000000ll);
                 A.out.req.evictions[g] = 0u;
-                serv = (long long)prompt + 1 <= T.cap;
-                A.w.flg[g] = serv ? ST_WAIT : ST_UNS;
             }
             unsigned sm_ = __ballot_sync(FULL, v && serv), um = __ballot_sync(FULL, v && !serv);
             if (v && serv) A.w.pend[T.off + T.npend + __popc(sm_ & lt)] = (uint32_t)i;
-            if (v && !serv) A.out.unservable_slots[T.off + T.nuns + __popc(um & lt)] = (uint32_t)i;
+            if (v && !serv) A.out.unservable_slots[T.off + nuns + __popc(um & lt)] = (uint32_t)i;
             T.npend += __popc(sm_);
-            T.nuns += __popc(um);
+            nuns += __popc(um);
         }
+        if (lane == 0) c.nuns = nuns;
         T.cursor = 0;
         __syncwarp();
+        T.next_ready = T.npend > 0 ? A.in.ready_time[T.off + A.w.pend[T.off]] : INFINITY;
 
-        MemS om;   // ongoing member copy held by this lane (lane < nO)
-        Key okey;  // its dispatch key
-        om.slot = 0;
+        Key okey;  // key of the ongoing record in OM[lane] (lane < nO)
 
         // ---- the round loop (engine.py:202-224)
         while (T.status == SS_TRACE_OK) {
             // admission of prediction-ready requests (engine.py:204-206)
-            {
-                double thr = ss::add(T.clock, 1e-12);
+            const double thr = ss::add(T.clock, 1e-12);
+            if (T.next_ready <= thr) {
                 while (T.cursor < T.npend) {
                     int i = T.cursor + lane;
                     bool v = i < T.npend;
@@ -628,37 +663,41 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                     Key k;
                     if (mine) {
                         long long g = T.off + s;
-                        A.w.flg[g] = ST_WAIT | F_Q;
-                        k = make_key<POL>(__ldg(A.in.pred_urgency + g), A.w.ft[g], __ldg(A.in.tie_rank + g), s, false);
+                        *FLG(A, g) = ST_WAIT | F_Q;
+                        const uint32_t w = STA(A)[g].w;
+                        k = make_key<POL>(w >> 24, DYN(A)[g].ft, w & SLOT_MASK, s, false);
                     }
                     q_insert32<POL>(E, T, k, mine);
                     T.cursor += cnt;
                     if (cnt < 32) break;
                 }
+                T.next_ready = T.cursor < T.npend ? A.in.ready_time[T.off + A.w.pend[T.off + T.cursor]] : INFINITY;
             }
-            int live = T.nF + T.nB + T.nO;
+            const int live = T.nF + T.nB + T.nO;
             if (live == 0) {
                 if (T.cursor >= T.npend) break;
-                T.clock = A.in.ready_time[T.off + A.w.pend[T.off + T.cursor]];
+                T.clock = T.next_ready;
                 continue;
             }
             if (T.nF < b && T.nB > 0) refill(E, T);
-            T.s_pool += live;
+            if (lane == 0) c.s_pool += live;
 
             // ---- stage-aware composition (batching.py:46-88)
             const int nc = T.nF < b ? T.nF : b;
             const bool has_c = lane < nc;
             const bool has_o = lane < T.nO;
-            Key ck;   // candidate's key: stored (fast path) or current (general path)
-            MemS cm;
+            Key ck;  // candidate key: stored (fast path) or current (general path)
             if (has_c) {
                 ck = sm->F[lane];
-                load_mem(A, T.off, ck.aux & SLOT_MASK, cm);  // used if selected
-                if (anom) ck = make_key<POL>(cm.urank, cm.ft, cm.tie, cm.slot, (cm.flg & F_STAGE) == ST_DEC);
+                if (anom) {
+                    MemS cm;
+                    load_mem(A, T.off, ck.aux & SLOT_MASK, cm);
+                    ck = mem_key<POL>(cm);
+                }
             }
-            // p* = min over candidates and ongoing (current keys). The ongoing
-            // copies are kept sorted by key across lanes (order among them is
-            // unobservable in the reference: equal keys are the same request).
+            // p* = min over candidates and ongoing (current keys); the ongoing
+            // copies are sorted by key across lanes (their order is unobservable
+            // in the reference: equal keys are copies of the same request)
             Key pmin = kinf();
             if (!anom) {
                 if (T.nO > 0) pmin = kshfl(okey, 0);
@@ -678,7 +717,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
             const unsigned cmask = __ballot_sync(FULL, c_elig);
             int cnt_c = 0, cnt_o = 0;
             if (!anom) {
-                // both lists sorted: ranks are own index + lower_bound in the other
+                // both lists sorted: rank = own index + lower_bound in the other
                 cnt_o = lane;
                 if (cmask) {
                     if (has_o) sm->X[32 + lane] = okey;
@@ -721,33 +760,37 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                     if (has_o && (klt(x, okey) || (keq(x, okey) && k < lane))) cnt_o++;
                 }
             }
-            const int c_rank = cnt_c;
             const int elig = __popc(cmask) + T.nO;
             const int m = elig < b ? elig : b;
-            const bool c_sel = c_elig && c_rank < m;
+            const bool c_sel = c_elig && cnt_c < m;
             Round R;
             R.G = 0;
             R.evmask = 0;
             R.ndec = 0;
             R.dpend = 0ull;
             R.rmF = (unsigned long long)__ballot_sync(FULL, c_sel);
+            // batch members -> M[rank]; the common decode round (batch == ongoing
+            // in order) reads its records straight from OM
+            const bool direct = cmask == 0 && T.nO <= b;
             __syncwarp();
             if (c_sel) {
-                // popped from the heap for good: no longer queued
-                cm.flg &= ~F_Q;
-                A.w.flg[T.off + cm.slot] = cm.flg;
-                sm->M[c_rank] = cm;
+                MemS cm;
+                load_mem(A, T.off, ck.aux & SLOT_MASK, cm);
+                cm.flg &= ~F_Q;  // popped from the heap for good
+                *FLG(A, T.off + cm.slot) = cm.flg;
+                sm->M[cnt_c] = cm;
             }
-            if (has_o && cnt_o < m) sm->M[cnt_o] = om;
+            if (!direct && has_o && cnt_o < m) sm->M[cnt_o] = sm->OM[lane];
             if (anom) {
                 // candidates not selected are pushed back with their current key;
                 // a stale stored key is replaced (heaps.py insert after pop)
-                bool refresh = has_c && !c_sel && !keq(ck, sm->F[lane]);
-                unsigned rm2 = __ballot_sync(FULL, refresh);
+                const bool refresh = has_c && !c_sel && !keq(ck, sm->F[lane]);
+                const unsigned rm2 = __ballot_sync(FULL, refresh);
                 R.rmF |= (unsigned long long)rm2;
                 if (refresh) {
+                    const uint32_t s = ck.aux & SLOT_MASK;
                     INS(A)[T.off + T.nins + __popc(rm2 & lt)] = ck;
-                    A.w.flg[T.off + cm.slot] = cm.flg | F_INS;
+                    *FLG(A, T.off + s) = *FLG(A, T.off + s) | F_INS;
                 }
                 T.nins += __popc(rm2);
                 __syncwarp();
@@ -755,27 +798,28 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                 // DuplicateRequestError in the reference (heaps.py:49-51)
                 unsigned pm = __ballot_sync(FULL, has_o && cnt_o >= m);
                 while (pm) {
-                    int k = __ffs(pm) - 1;
+                    const int k = __ffs(pm) - 1;
                     pm &= pm - 1;
-                    uint32_t s = __shfl_sync(FULL, om.slot, k);
-                    uint32_t f = A.w.flg[T.off + s];
+                    const uint32_t s = sm->OM[k].slot;
+                    const uint32_t f = *FLG(A, T.off + s);
                     if (f & F_Q) {
                         set_status(T, SS_TRACE_REF_ERROR);
                         break;
                     }
-                    Key kk = kshfl(okey, k);
+                    const Key kk = kshfl(okey, k);
                     if (lane == 0) {
-                        A.w.flg[T.off + s] = f | F_Q | F_INS;
+                        *FLG(A, T.off + s) = f | F_Q | F_INS;
                         INS(A)[T.off + T.nins] = kk;
                     }
                     T.nins += 1;
                     __syncwarp();
                 }
             } else {
-                bool pushed = has_o && cnt_o >= m;
-                unsigned pm = __ballot_sync(FULL, pushed);
+                const bool pushed = has_o && cnt_o >= m;
+                const unsigned pm = __ballot_sync(FULL, pushed);
                 if (pushed) {
-                    A.w.flg[T.off + om.slot] = om.flg | F_Q | F_INS;
+                    const MemS& o = sm->OM[lane];
+                    *FLG(A, T.off + o.slot) = o.flg | F_Q | F_INS;
                     INS(A)[T.off + T.nins + __popc(pm & lt)] = okey;
                 }
                 T.nins += __popc(pm);
@@ -786,13 +830,13 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
             mem.slot = 0xFFFFFFFFu;
             const bool act = lane < m;
             if (act) {
-                mem = sm->M[lane];
-                if (anom) mem.flg = A.w.flg[T.off + mem.slot];  // queued bit may have moved
+                mem = direct ? sm->OM[lane] : sm->M[lane];
+                if (anom) mem.flg = *FLG(A, T.off + mem.slot);  // queued bit may have moved
             }
             const int nO_start = T.nO;
-            const int nuns_start = T.nuns;
+            const int nuns_start = c.nuns;
             // a completed request popped from a stale entry: estimate_kv_size raises
-            if (__ballot_sync(FULL, act && (mem.flg & F_STAGE) == ST_DONE)) {
+            if (anom && __ballot_sync(FULL, act && (mem.flg & F_STAGE) == ST_DONE)) {
                 set_status(T, SS_TRACE_REF_ERROR);
                 break;
             }
@@ -800,42 +844,38 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
             // ---- admission with KV budget (engine.py:296-327)
             MemQ q = mem_q(mem);
             {
-                long long excl;
+                int excl;
                 if (__all_sync(FULL, !act || q.isdec)) {
                     excl = lane;  // every immediate is 1
                 } else {
-                    int inc = act ? (int)q.imm : 0;
+                    const int inc = act ? (int)q.imm : 0;
                     int sc = inc;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         int tt = __shfl_up_sync(FULL, sc, o);
                         if (lane >= o) sc += tt;
                     }
-                    excl = (long long)(sc - inc);
+                    excl = sc - inc;
                 }
                 long long dem = q.est > q.imm ? q.est : q.imm;
-                if (dem + excl > T.cap) dem = q.imm;
-                bool need = act && (dem + excl + T.used > T.cap);
-                unsigned nm = __ballot_sync(FULL, need);
+                if (dem + excl > cap) dem = q.imm;
+                const bool need = act && (dem + excl + T.used > cap);
+                const unsigned nm = __ballot_sync(FULL, need);
                 const unsigned mmask = m >= 32 ? FULL : ((1u << m) - 1u);
                 const int f = nm ? __ffs(nm) - 1 : m;
-                R.G = f >= 32 ? FULL : ((1u << f) - 1u);
-                R.G &= mmask;
-                {
+                R.G = (f >= 32 ? FULL : ((1u << f) - 1u)) & mmask;
+                if (anom) {
                     // grants of still-queued requests (stale heap entry) before f
-                    unsigned qa = __ballot_sync(FULL, ((R.G >> lane) & 1u) && (mem.flg & F_Q));
-                    if (qa) {
-                        T.anomalies += __popc(qa);
-                        anom = true;
-                    }
+                    const unsigned qa = __ballot_sync(FULL, ((R.G >> lane) & 1u) && (mem.flg & F_Q));
+                    if (qa && lane == 0) c.anomalies += __popc(qa);
                 }
                 if (nm) {
-                    T.s_res += T.nR;
+                    if (lane == 0) c.s_res += T.nR;
                     // slow path: one member at a time from the first that must evict
                     long long reserved = __shfl_sync(FULL, excl, f);
                     if ((R.G >> lane) & 1u) {
                         mem.flg |= F_GRANT;
-                        A.w.flg[T.off + mem.slot] = mem.flg;
+                        *FLG(A, T.off + mem.slot) = mem.flg;
                     }
                     __syncwarp();
                     for (int k = f; k < m && T.status == SS_TRACE_OK; k++) {
@@ -846,13 +886,13 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                         const long long kvd_k = __shfl_sync(FULL, q.kvd, k);
                         const uint32_t slot_k = __shfl_sync(FULL, mem.slot, k);
                         long long dem_k = est_k > imm_k ? est_k : imm_k;
-                        if (dem_k + reserved > T.cap) dem_k = imm_k;
+                        if (dem_k + reserved > cap) dem_k = imm_k;
                         const long long demand = dem_k + reserved;
                         const int d0 = R.ndec;
                         unsigned vcall = 0;
                         R.dpend = 0ull;
                         bool ok = true;
-                        while (demand + T.used > T.cap) {
+                        while (demand + T.used > cap) {
                             if (!evict_one<POL>(E, T, R, slot_k, m, mem, vcall)) {
                                 ok = false;
                                 break;
@@ -861,14 +901,16 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                         const uint32_t flg_k = __shfl_sync(FULL, mem.flg, k);
                         if (!ok) {
                             // AdmissionFailure: evictions stand, their records are lost
-                            T.lost += R.ndec - d0;
+                            if (lane == 0) c.lost += R.ndec - d0;
                             R.ndec = d0;
-                            if (kvd_k + imm_k > T.cap) {
+                            if (kvd_k + imm_k > cap) {
                                 // _mark_unservable (engine.py:402-412)
                                 q_delete(E, T, R, slot_k, flg_k);
                                 const bool isdec_k = (flg_k & F_STAGE) == ST_DEC;
+                                const int un = c.nuns;
+                                __syncwarp();
                                 if (lane == k) {
-                                    long long g = T.off + mem.slot;
+                                    const long long g = T.off + mem.slot;
                                     if (isdec_k) {
                                         uint32_t ri = A.w.rpos[g];
                                         uint32_t last = A.w.R[T.off + T.nR - 1];
@@ -876,26 +918,25 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                                         A.w.rpos[T.off + last] = ri;
                                     }
                                     mem.flg = (mem.flg & ~(F_STAGE | F_Q | F_INS | F_GRANT)) | ST_UNS;
-                                    A.w.flg[g] = mem.flg;
-                                    A.out.unservable_slots[T.off + T.nuns] = mem.slot;
+                                    *FLG(A, g) = mem.flg;
+                                    A.out.unservable_slots[T.off + un] = mem.slot;
+                                    c.nuns = un + 1;
                                 }
                                 if (isdec_k) T.nR -= 1;
                                 T.used -= kvd_k;
-                                T.nuns += 1;
                                 __syncwarp();
                                 // other batch copies of it see the new state
-                                if (lane != k && act && mem.slot == slot_k) mem.flg = A.w.flg[T.off + slot_k];
+                                if (lane != k && act && mem.slot == slot_k) mem.flg = *FLG(A, T.off + slot_k);
                             } else if (!(flg_k & F_Q)) {
-                                Key kk;
                                 if (lane == k) {
-                                    kk = make_key<POL>(mem.urank, mem.ft, mem.tie, mem.slot, q.isdec);
+                                    const Key kk = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, q.isdec);
                                     mem.flg |= F_Q | F_INS;
-                                    A.w.flg[T.off + mem.slot] = mem.flg;
+                                    *FLG(A, T.off + mem.slot) = mem.flg;
                                     INS(A)[T.off + T.nins] = kk;
                                 }
                                 T.nins += 1;
                                 __syncwarp();
-                                if (lane != k && act && mem.slot == slot_k) mem.flg = A.w.flg[T.off + slot_k];
+                                if (lane != k && act && mem.slot == slot_k) mem.flg = *FLG(A, T.off + slot_k);
                             }
                             __syncwarp();
                             continue;
@@ -906,14 +947,14 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                         if (flg_k & F_Q) {
                             // granted while it still has a heap entry (a victim whose
                             // decision was lost): the reference keeps that stale entry
-                            T.anomalies += 1;
+                            if (lane == 0) c.anomalies += 1;
                             anom = true;
                         }
                         R.G |= 1u << k;
                         reserved += imm_k;
                         if (lane == k) {
                             mem.flg |= F_GRANT;
-                            A.w.flg[T.off + mem.slot] = mem.flg;
+                            *FLG(A, T.off + mem.slot) = mem.flg;
                         }
                         __syncwarp();
                         if (act && lane != k && mem.slot == slot_k) mem.flg |= F_GRANT;
@@ -921,49 +962,50 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                 }
             }
             if (T.status != SS_TRACE_OK) break;
-            T.evictions += R.ndec;
             const bool g_act = (R.G >> lane) & 1u;
             const int ng = __popc(R.G);
-            T.s_granted += ng;
             const unsigned long long r64 = (unsigned long long)T.rounds;
+            if (lane == 0) {
+                c.evictions += R.ndec;
+                c.s_granted += ng;
+            }
 
             if (ng == 0) {
                 // nothing granted (engine.py:329-344): clock does not advance
                 T.nO = 0;
-                if ((A.P.flags & SS_FLAG_DIGEST) && lane == 0) {
+                if (want_digest && lane == 0) {
                     dig += ss_term(r64, SS_TAG_HDR, 0, ss_hdr_word(SS_KIND_NONE, 0, 0, R.ndec));
                     dig += ss_term(r64, SS_TAG_MEM, 0, (unsigned long long)T.used);
                     dig += ss_term(r64, SS_TAG_TIME, 0, dbits(T.clock));
                 }
-                if (R.ndec > 0) {
-                    if (T.used > T.peak) T.peak = T.used;
-                    if (T.log) {
-                        if (lane == 0) {
-                            unsigned long long mu = (unsigned long long)T.used, tb = dbits(T.clock);
-                            log_put(T, T.logpos + 0, SS_KIND_NONE);
-                            log_put(T, T.logpos + 1, 0);
-                            log_put(T, T.logpos + 2, 0);
-                            log_put(T, T.logpos + 3, (uint32_t)R.ndec);
-                            log_put(T, T.logpos + 4, (uint32_t)mu);
-                            log_put(T, T.logpos + 5, (uint32_t)(mu >> 32));
-                            log_put(T, T.logpos + 6, (uint32_t)tb);
-                            log_put(T, T.logpos + 7, (uint32_t)(tb >> 32));
-                        }
-                        T.logpos += SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * R.ndec;
+                if (R.ndec > 0 && lane == 0) {
+                    if (T.used > c.peak) c.peak = T.used;
+                    if (c.log) {
+                        const unsigned long long mu = (unsigned long long)T.used, tb = dbits(T.clock);
+                        log_put(c, c.logpos + 0, SS_KIND_NONE);
+                        log_put(c, c.logpos + 1, 0);
+                        log_put(c, c.logpos + 2, 0);
+                        log_put(c, c.logpos + 3, (uint32_t)R.ndec);
+                        log_put(c, c.logpos + 4, (uint32_t)mu);
+                        log_put(c, c.logpos + 5, (uint32_t)(mu >> 32));
+                        log_put(c, c.logpos + 6, (uint32_t)tb);
+                        log_put(c, c.logpos + 7, (uint32_t)(tb >> 32));
+                        c.logpos += SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * R.ndec;
                     }
                 }
                 T.rounds += 1;
-                if (R.ndec == 0 && T.nuns == nuns_start && nO_start == 0) set_status(T, SS_TRACE_LIVELOCK);
+                __syncwarp();
+                if (R.ndec == 0 && c.nuns == nuns_start && nO_start == 0) set_status(T, SS_TRACE_LIVELOCK);
             } else {
                 // ---- batch_duration (engine.py:126-149) over granted copies
                 q = mem_q(mem);
                 double total = 0.0;
                 const unsigned pre = __ballot_sync(FULL, g_act && !q.isdec);
                 if (pre) {
-                    double rl = reload_time(q.kvh, P);
-                    double pft = prefill_time((long long)mem.prompt - q.pfn, P);
+                    const double rl = reload_time(q.kvh, P);
+                    const double pft = prefill_time((long long)m_prompt(mem) - q.pfn, P);
                     for (int k = 0; k < m; k++) {
-                        double a = __shfl_sync(FULL, rl, k), c2 = __shfl_sync(FULL, pft, k);
+                        const double a = __shfl_sync(FULL, rl, k), c2 = __shfl_sync(FULL, pft, k);
                         if ((pre >> k) & 1u) {
                             total = ss::add(total, a);
                             total = ss::add(total, c2);
@@ -976,16 +1018,17 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                     if (!A.P.decode_cost_sum) {
                         // gamma1 >= 0: the step time is monotone in the context length,
                         // so the max step is the step of the longest context
-                        unsigned nmax = __reduce_max_sync(FULL, (g_act && q.isdec) ? mem.prompt + mem.dec + 1u : 0u);
+                        const unsigned nmax =
+                            __reduce_max_sync(FULL, (g_act && q.isdec) ? m_prompt(mem) + mem.dec + 1u : 0u);
                         part = decode_step_time((long long)nmax, 1, P);
                     } else {
-                        double st = (g_act && q.isdec)
-                                        ? decode_step_time((long long)mem.prompt + mem.dec + 1, 1, P)
-                                        : 0.0;
+                        const double st = (g_act && q.isdec)
+                                              ? decode_step_time((long long)m_prompt(mem) + mem.dec + 1, 1, P)
+                                              : 0.0;
                         PySum ps;
                         ps.init();
                         for (int k = 0; k < m; k++) {
-                            double x = __shfl_sync(FULL, st, k);
+                            const double x = __shfl_sync(FULL, st, k);
                             if ((dm >> k) & 1u) ps.push(x);
                         }
                         part = ps.value();
@@ -996,13 +1039,16 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
 
                 // ---- per-member progress (engine.py:351-363, 382-421)
                 bool done = false;
-                const unsigned dupm = __match_any_sync(FULL, g_act ? mem.slot : (0x80000000u | lane));
-                const bool dups = __ballot_sync(FULL, g_act && __popc(dupm) > 1) != 0;
+                bool dups = false;
+                if (anom) {
+                    const unsigned dupm = __match_any_sync(FULL, g_act ? mem.slot : (0x80000000u | lane));
+                    dups = __ballot_sync(FULL, g_act && __popc(dupm) > 1) != 0;
+                }
                 if (!dups) {
-                    long long delta = 0;
+                    int delta = 0;
                     bool newres = false;
                     if (g_act) {
-                        long long g = T.off + mem.slot;
+                        const long long g = T.off + mem.slot;
                         if (!(mem.flg & F_FIRST)) {
                             A.out.req.first_scheduled[g] = T.clock;
                             mem.flg |= F_FIRST;
@@ -1011,61 +1057,64 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                             delta = 1;
                             mem.dec += 1;
                         } else {
-                            delta = q.kvh + ((long long)mem.prompt - q.pfn);
+                            delta = (int)(q.kvh + (m_prompt(mem) - q.pfn));
                             mem.flg = (mem.flg & ~F_STAGE) | ST_DEC | F_PF;
                             newres = true;
                         }
                         mem.flg &= ~F_GRANT;
-                        if (mem.dec >= mem.tout) {
+                        if (mem.dec >= m_tout(mem)) {
                             done = true;
-                            delta -= (long long)mem.prompt + mem.dec;
+                            delta -= (int)(m_prompt(mem) + mem.dec);
                             A.out.req.finish_time[g] = end;
                             mem.ft = 0.0;
                             mem.flg = (mem.flg & ~F_STAGE) | ST_DONE;
                         } else {
-                            mem.ft = remaining_time(mem.prompt, mem.mid, mem.prompt, mem.dec, 0, P);
+                            mem.ft = remaining_time(m_prompt(mem), m_mid(mem), m_prompt(mem), mem.dec, 0, P);
                         }
-                        A.w.dec[g] = mem.dec;
-                        A.w.ft[g] = mem.ft;
-                        A.w.flg[g] = mem.flg;
+                        store_dyn(A, g, mem.ft, mem.dec, mem.flg);
                     }
                     // allocations all fit (admission reserved them); completions release
-                    T.used += (long long)__reduce_add_sync(FULL, (int)delta);
-                    if (T.used > T.cap || T.used < 0) set_status(T, SS_TRACE_INTERNAL);
-                    const unsigned nm = __ballot_sync(FULL, newres);
-                    if (newres) {
-                        uint32_t idx = (uint32_t)(T.nR + __popc(nm & lt));
-                        A.w.R[T.off + idx] = mem.slot;
-                        A.w.rpos[T.off + mem.slot] = idx;
-                    }
-                    T.nR += __popc(nm);
-                    unsigned cmk = __ballot_sync(FULL, done);
-                    __syncwarp();
-                    while (cmk) {
-                        int k = __ffs(cmk) - 1;
-                        cmk &= cmk - 1;
-                        uint32_t s = __shfl_sync(FULL, mem.slot, k);
-                        if (lane == 0) {
-                            uint32_t ri = A.w.rpos[T.off + s];
-                            uint32_t last = A.w.R[T.off + T.nR - 1];
-                            A.w.R[T.off + ri] = last;
-                            A.w.rpos[T.off + last] = ri;
+                    T.used += (long long)__reduce_add_sync(FULL, delta);
+                    if (T.used > cap || T.used < 0) set_status(T, SS_TRACE_INTERNAL);
+                    const unsigned nmr = __ballot_sync(FULL, newres);
+                    if (nmr) {
+                        if (newres) {
+                            const uint32_t idx = (uint32_t)(T.nR + __popc(nmr & lt));
+                            A.w.R[T.off + idx] = mem.slot;
+                            A.w.rpos[T.off + mem.slot] = idx;
                         }
-                        T.nR -= 1;
+                        T.nR += __popc(nmr);
+                    }
+                    unsigned cmk = __ballot_sync(FULL, done);
+                    if (cmk) {
                         __syncwarp();
+                        while (cmk) {
+                            const int k = __ffs(cmk) - 1;
+                            cmk &= cmk - 1;
+                            const uint32_t s = __shfl_sync(FULL, mem.slot, k);
+                            if (lane == 0) {
+                                const uint32_t ri = A.w.rpos[T.off + s];
+                                const uint32_t last = A.w.R[T.off + T.nR - 1];
+                                A.w.R[T.off + ri] = last;
+                                A.w.rpos[T.off + last] = ri;
+                            }
+                            T.nR -= 1;
+                            __syncwarp();
+                        }
                     }
                 } else {
                     // duplicate copies of a request: execute copies one by one,
                     // each seeing the previous copy's effect
                     unsigned gm = R.G;
                     while (gm && T.status == SS_TRACE_OK) {
-                        int k = __ffs(gm) - 1;
+                        const int k = __ffs(gm) - 1;
                         gm &= gm - 1;
                         int err = 0, dn = 0, nres = 0;
                         long long alloc = 0, rel = 0;
                         if (lane == k) {
-                            long long g = T.off + mem.slot;
-                            uint32_t dec = A.w.dec[g], fl = A.w.flg[g];
+                            const long long g = T.off + mem.slot;
+                            const Dyn d = DYN(A)[g];
+                            uint32_t dec = d.dec, fl = d.flg;
                             if ((fl & F_STAGE) == ST_DONE) {
                                 err = 1;  // transition(PREFILLING) from COMPLETED
                             } else {
@@ -1077,25 +1126,23 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                                     alloc = 1;
                                     dec += 1;
                                 } else {
-                                    long long pfn = (fl & F_PF) ? (long long)mem.prompt : 0;
-                                    alloc = pfn + dec + ((long long)mem.prompt - pfn);
+                                    const long long pfn = (fl & F_PF) ? (long long)m_prompt(mem) : 0;
+                                    alloc = pfn + dec + ((long long)m_prompt(mem) - pfn);
                                     fl = (fl & ~F_STAGE) | ST_DEC | F_PF;
                                     nres = 1;
                                 }
                                 fl &= ~F_GRANT;
                                 double ft;
-                                if (dec >= mem.tout) {
+                                if (dec >= m_tout(mem)) {
                                     dn = 1;
-                                    rel = (long long)mem.prompt + dec;
+                                    rel = (long long)m_prompt(mem) + dec;
                                     A.out.req.finish_time[g] = end;
                                     ft = 0.0;
                                     fl = (fl & ~F_STAGE) | ST_DONE;
                                 } else {
-                                    ft = remaining_time(mem.prompt, mem.mid, mem.prompt, dec, 0, P);
+                                    ft = remaining_time(m_prompt(mem), m_mid(mem), m_prompt(mem), dec, 0, P);
                                 }
-                                A.w.dec[g] = dec;
-                                A.w.ft[g] = ft;
-                                A.w.flg[g] = fl;
+                                store_dyn(A, g, ft, dec, fl);
                             }
                         }
                         err = __shfl_sync(FULL, err, k);
@@ -1104,24 +1151,22 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                         alloc = __shfl_sync(FULL, alloc, k);
                         rel = __shfl_sync(FULL, rel, k);
                         const uint32_t s = __shfl_sync(FULL, mem.slot, k);
-                        if (err || alloc > T.cap - T.used) {
+                        if (err || alloc > cap - T.used) {
                             set_status(T, SS_TRACE_REF_ERROR);
                             break;
                         }
                         T.used += alloc;
                         if (lane == k) done = dn != 0;
-                        if (lane == 0) {
-                            if (nres) {
-                                A.w.R[T.off + T.nR] = s;
-                                A.w.rpos[T.off + s] = (uint32_t)T.nR;
-                            }
+                        if (lane == 0 && nres) {
+                            A.w.R[T.off + T.nR] = s;
+                            A.w.rpos[T.off + s] = (uint32_t)T.nR;
                         }
                         if (nres) T.nR += 1;
                         __syncwarp();
                         if (dn) {
                             if (lane == 0) {
-                                uint32_t ri = A.w.rpos[T.off + s];
-                                uint32_t last = A.w.R[T.off + T.nR - 1];
+                                const uint32_t ri = A.w.rpos[T.off + s];
+                                const uint32_t last = A.w.R[T.off + T.nR - 1];
                                 A.w.R[T.off + ri] = last;
                                 A.w.rpos[T.off + last] = ri;
                             }
@@ -1132,76 +1177,82 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                     }
                     if (T.status != SS_TRACE_OK) break;
                     if (g_act) {  // every copy sees the final state
-                        long long g = T.off + mem.slot;
-                        mem.dec = A.w.dec[g];
-                        mem.flg = A.w.flg[g];
-                        mem.ft = A.w.ft[g];
+                        const Dyn d = DYN(A)[T.off + mem.slot];
+                        mem.dec = d.dec;
+                        mem.flg = d.flg;
+                        mem.ft = d.ft;
                     }
                 }
                 // ---- ITERATION_END record (engine.py:365-380) + digest
                 const unsigned cdone = __ballot_sync(FULL, done);
                 const int nc_done = __popc(cdone);
                 const int gi = __popc(R.G & lt), ci = __popc(cdone & lt);
-                if (A.P.flags & SS_FLAG_DIGEST) {
+                if (want_digest) {
                     if (g_act) dig += ss_term(r64, SS_TAG_GRANT, gi, mem.slot);
                     if (done) dig += ss_term(r64, SS_TAG_DONE, ci, mem.slot);
                     if (lane == 31) dig += ss_term(r64, SS_TAG_HDR, 0, ss_hdr_word(kind, ng, nc_done, R.ndec));
                     if (lane == 30) dig += ss_term(r64, SS_TAG_MEM, 0, (unsigned long long)T.used);
                     if (lane == 29) dig += ss_term(r64, SS_TAG_TIME, 0, dbits(end));
                 }
-                if (T.log) {
-                    long long base = T.logpos + SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * R.ndec;
-                    if (g_act) log_put(T, base + gi, mem.slot);
-                    if (done) log_put(T, base + ng + ci, mem.slot);
+                if (logging) {
+                    const long long lp = c.logpos;
+                    const long long base = lp + SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * R.ndec;
+                    if (g_act) log_put(c, base + gi, mem.slot);
+                    if (done) log_put(c, base + ng + ci, mem.slot);
+                    __syncwarp();
                     if (lane == 0) {
-                        unsigned long long mu = (unsigned long long)T.used, tb = dbits(end);
-                        log_put(T, T.logpos + 0, (uint32_t)kind);
-                        log_put(T, T.logpos + 1, (uint32_t)ng);
-                        log_put(T, T.logpos + 2, (uint32_t)nc_done);
-                        log_put(T, T.logpos + 3, (uint32_t)R.ndec);
-                        log_put(T, T.logpos + 4, (uint32_t)mu);
-                        log_put(T, T.logpos + 5, (uint32_t)(mu >> 32));
-                        log_put(T, T.logpos + 6, (uint32_t)tb);
-                        log_put(T, T.logpos + 7, (uint32_t)(tb >> 32));
+                        const unsigned long long mu = (unsigned long long)T.used, tb = dbits(end);
+                        log_put(c, lp + 0, (uint32_t)kind);
+                        log_put(c, lp + 1, (uint32_t)ng);
+                        log_put(c, lp + 2, (uint32_t)nc_done);
+                        log_put(c, lp + 3, (uint32_t)R.ndec);
+                        log_put(c, lp + 4, (uint32_t)mu);
+                        log_put(c, lp + 5, (uint32_t)(mu >> 32));
+                        log_put(c, lp + 6, (uint32_t)tb);
+                        log_put(c, lp + 7, (uint32_t)(tb >> 32));
+                        c.logpos = base + ng + nc_done;
                     }
-                    T.logpos = base + ng + nc_done;
                 }
-                if (T.used > T.peak) T.peak = T.used;
+                if (lane == 0 && T.used > c.peak) c.peak = T.used;
                 T.clock = end;
                 T.rounds += 1;
                 // ---- ongoing = granted copies not completed, in granted order
                 const bool stay = g_act && (mem.flg & F_STAGE) != ST_DONE;
                 const unsigned smk = __ballot_sync(FULL, stay);
                 __syncwarp();
-                if (stay) sm->M[__popc(smk & lt)] = mem;
-                __syncwarp();
+                if (stay) sm->OM[__popc(smk & lt)] = mem;
                 T.nO = __popc(smk);
-                if (lane < T.nO) {
-                    om = sm->M[lane];
-                    okey = make_key<POL>(om.urank, om.ft, om.tie, om.slot, true);
+                __syncwarp();
+                const bool prefix = smk == FULL || smk == (1u << __popc(smk)) - 1u;
+                if (stay && prefix) {
+                    okey = mem_key<POL>(mem);  // no compaction: lane keeps its record
+                } else if (lane < T.nO) {
+                    okey = mem_key<POL>(sm->OM[lane]);
                 }
-                // keep the ongoing copies sorted by their new keys (usually they are)
+                // keep the ongoing records sorted by their new keys (usually they are)
                 {
-                    Key nk = kshfl_down(okey, 1);
+                    const Key nk = kshfl_down(okey, 1);
                     if (__ballot_sync(FULL, lane + 1 < T.nO && klt(nk, okey))) {
                         if (lane < T.nO) sm->X[32 + lane] = okey;
                         __syncwarp();
                         int r = 0;
                         for (int k = 0; k < T.nO; k++) {
-                            Key x = sm->X[32 + k];
+                            const Key x = sm->X[32 + k];
                             if (klt(x, okey) || (keq(x, okey) && k < lane)) r++;
                         }
+                        MemS mine;
+                        if (lane < T.nO) mine = sm->OM[lane];
                         __syncwarp();
-                        if (lane < T.nO) sm->M[r] = om;
+                        if (lane < T.nO) sm->OM[r] = mine;
                         __syncwarp();
-                        if (lane < T.nO) {
-                            om = sm->M[lane];
-                            okey = make_key<POL>(om.urank, om.ft, om.tie, om.slot, true);
-                        }
+                        if (lane < T.nO) okey = mem_key<POL>(sm->OM[lane]);
                     }
                 }
             }
-            if (T.log && T.logpos > T.logcap) set_status(T, SS_TRACE_LOG_OVERFLOW);
+            if (logging) {
+                __syncwarp();
+                if (c.logpos > c.logcap) set_status(T, SS_TRACE_LOG_OVERFLOW);
+            }
             if (A.P.max_rounds > 0 && T.rounds >= A.P.max_rounds) set_status(T, SS_TRACE_ROUND_CAP);
 
             // ---- queue rebuild: drop popped FRONT entries, then insert this
@@ -1209,55 +1260,52 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
             //      they were queued with (the heap stores keys at insert time)
             f_compact(E, T, R.rmF);
             for (int base = 0; base < T.nins; base += 32) {
-                int i = base + lane;
+                const int i = base + lane;
                 bool v = false;
                 Key k;
                 if (i < T.nins) {
                     k = INS(A)[T.off + i];
-                    uint32_t s = k.aux & SLOT_MASK;
+                    const uint32_t s = k.aux & SLOT_MASK;
                     if (s != SLOT_MASK) {
-                        long long g = T.off + s;
-                        uint32_t f = A.w.flg[g];
                         v = true;
-                        A.w.flg[g] = f & ~F_INS;
+                        uint32_t* fp = FLG(A, T.off + s);
+                        *fp = *fp & ~F_INS;
                     }
                 }
                 q_insert32<POL>(E, T, k, v);
             }
             T.nins = 0;
-            __syncwarp();
         }
 
         // ---- outputs and the fused statistics (metrics.py:35-56)
         {
             PySum acc;
             acc.init();
-            for (int base = 0; base < T.n; base += 32) {
-                int i = base + lane;
-                bool v = i < T.n;
+            for (int base = 0; base < n; base += 32) {
+                const int i = base + lane;
                 double w = 0.0, nw = 0.0;
                 bool fin = false;
                 int lv = 0;
-                if (v) {
-                    long long g = T.off + i;
-                    uint32_t f = A.w.flg[g], dcount = A.w.dec[g];
-                    A.out.req.generated[g] = dcount;
-                    if (A.out.req.f_t) A.out.req.f_t[g] = A.w.ft[g];
-                    if (A.out.req.state) A.out.req.state[g] = (f & F_STAGE) | ((f & F_PF) ? 256u : 0u);
-                    double fi = A.out.req.finish_time[g];
+                if (i < n) {
+                    const long long g = T.off + i;
+                    const Dyn d = DYN(A)[g];
+                    A.out.req.generated[g] = d.dec;
+                    if (A.out.req.f_t) A.out.req.f_t[g] = d.ft;
+                    if (A.out.req.state) A.out.req.state[g] = (d.flg & F_STAGE) | ((d.flg & F_PF) ? 256u : 0u);
+                    const double fi = A.out.req.finish_time[g];
                     if (!isnan(fi)) {
                         fin = true;
                         w = ss::sub(fi, A.in.arrival_time[g]);
-                        nw = ss::dv(w, (double)dcount);
+                        nw = ss::dv(w, (double)d.dec);
                         lv = A.in.true_urgency[g];
                     }
                 }
                 unsigned fm = __ballot_sync(FULL, fin);
                 while (fm) {
-                    int k = __ffs(fm) - 1;
+                    const int k = __ffs(fm) - 1;
                     fm &= fm - 1;
-                    double wk = __shfl_sync(FULL, w, k), nk = __shfl_sync(FULL, nw, k);
-                    int lk = __shfl_sync(FULL, lv, k);
+                    const double wk = __shfl_sync(FULL, w, k), nk = __shfl_sync(FULL, nw, k);
+                    const int lk = __shfl_sync(FULL, lv, k);
                     if (lane == 31) acc.push(wk);
                     else if (lane == 30) acc.push(nk);
                     else if (lane == lk && lane < SS_MAX_LEVELS) acc.push(nk);
@@ -1278,20 +1326,20 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                 st->completed = cntv;
             }
             if (lane == 0) {
-                st->digest = (A.P.flags & SS_FLAG_DIGEST) ? dig : 0ull;
+                st->digest = want_digest ? dig : 0ull;
                 st->rounds = T.rounds;
-                st->evictions = T.evictions;
-                st->mem_used_peak = T.peak;
-                st->log_words = T.log ? (T.logpos < T.logcap ? T.logpos : T.logcap) : 0;
-                st->unservable = T.nuns;
+                st->evictions = c.evictions;
+                st->mem_used_peak = c.peak;
+                st->log_words = c.log ? (c.logpos < c.logcap ? c.logpos : c.logcap) : 0;
+                st->unservable = c.nuns;
                 st->status = T.status;
-                st->lost_evictions = T.lost;
-                st->anomalies = T.anomalies;
+                st->lost_evictions = c.lost;
+                st->anomalies = c.anomalies;
                 st->_pad = 0;
-                st->sum_pool = T.s_pool;
-                st->sum_granted = T.s_granted;
-                st->sum_victims = T.s_victims;
-                st->sum_resident_evict = T.s_res;
+                st->sum_pool = c.s_pool;
+                st->sum_granted = c.s_granted;
+                st->sum_victims = c.s_victims;
+                st->sum_resident_evict = c.s_res;
                 st->final_clock = T.clock;
             }
         }
@@ -1306,20 +1354,20 @@ static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 size_t work_bytes(int64_t n) {
     size_t nn = (size_t)(n > 0 ? n : 1);
-    return align16(nn * 8) + 4 * align16(nn * 4) + 2 * align16(nn * 16) + align16(nn * 4) + 16;
+    // st, dy, B, ins: 16 B; rpos, R, pend: 4 B
+    return 4 * align16(nn * 16) + 3 * align16(nn * 4) + 16;
 }
 
 void carve_work(void* base, int64_t n, Work* w) {
     size_t nn = (size_t)(n > 0 ? n : 1);
     char* p = (char*)base;
-    w->ft = (double*)p;      p += align16(nn * 8);
-    w->dec = (uint32_t*)p;   p += align16(nn * 4);
-    w->flg = (uint32_t*)p;   p += align16(nn * 4);
+    w->st = (void*)p;        p += align16(nn * 16);
+    w->dy = (void*)p;        p += align16(nn * 16);
+    w->B = (void*)p;         p += align16(nn * 16);
+    w->ins = (void*)p;       p += align16(nn * 16);
     w->rpos = (uint32_t*)p;  p += align16(nn * 4);
     w->R = (uint32_t*)p;     p += align16(nn * 4);
-    w->B = (void*)p;         p += align16(nn * 16);
     w->pend = (uint32_t*)p;  p += align16(nn * 4);
-    w->ins = (void*)p;       p += align16(nn * 16);
     w->next_trace = (int*)p;
 }
 
@@ -1341,6 +1389,7 @@ int sched_max_blocks(int policy, int* sm_count) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const void* k = kernel_for(policy);
     if (!k) return 0;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sched_smem_bytes());
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 32 * WPB, sched_smem_bytes());
     if (sm_count) *sm_count = sms;
     return per * sms;

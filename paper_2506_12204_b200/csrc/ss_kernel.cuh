@@ -11,9 +11,8 @@ constexpr int WPB = 4;    // traces (warps) per CTA
 
 // Per-request scratch in HBM, indexed like the inputs (trace offset + slot).
 struct Work {
-    double* ft;          // current f_t (Request.f_t)
-    uint32_t* dec;       // decoded tokens
-    uint32_t* flg;       // stage | prefilled | queued | in-insert-list | first-set | granted
+    void* st;            // static record: prompt, true_out, pred_len, rank << 24 | tie
+    void* dy;            // dynamic record: f_t, decoded, flags (stage | prefilled | queued | ...)
     uint32_t* rpos;      // position in the resident list
     void* B;             // queue BACK: 16-byte packed keys
     uint32_t* R;         // resident list (eviction candidates)
