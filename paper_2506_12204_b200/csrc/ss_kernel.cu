@@ -39,7 +39,7 @@
 #define SS_EVICT_INLINE __device__ __forceinline__
 #endif
 #ifndef SS_MINB
-#define SS_MINB 1  // min resident CTAs per SM requested from ptxas (register cap)
+#define SS_MINB 4  // min resident CTAs per SM requested from ptxas (register cap: 128)
 #endif
 
 namespace ss {
