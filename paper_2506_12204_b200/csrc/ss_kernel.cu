@@ -74,6 +74,7 @@ struct __align__(16) Dyn {
 // trace state touched once per round or less: shared memory, lane 0 writes
 struct Cold {
     long long evictions, peak, s_pool, s_granted, s_victims, s_res, logpos, logcap;
+    unsigned long long dpend;  // digest terms of the current eviction call
     uint32_t* log;
     int nuns, lost, anomalies, n;
 };
@@ -210,11 +211,15 @@ __device__ __forceinline__ uint32_t* FLG(const KArgs& A, long long g) { return &
 // ---- queue front / back maintenance --------------------------------------
 
 // Insert up to 32 keys (one per lane, `valid`) into the queue (FRONT+BACK).
-template <int POL>
-__device__ void q_insert32(const Env& E, Trace& T, Key key, bool valid) {
-    const KArgs& A = *E.A;
-    WarpSmem* sm = E.sm;
-    const int lane = E.lane;
+struct QState {
+    long long off;
+    int nF, nB;
+};
+__device__ __noinline__ int2 q_insert32(const KArgs* Ap, WarpSmem* sm, long long off, int nF, int nB, Key key,
+                                        bool valid) {
+    const KArgs& A = *Ap;
+    const int lane = threadIdx.x & 31;
+    QState T{off, nF, nB};
     const unsigned lt = lanemask_lt();
     Key fmax;
     bool have_f = T.nF > 0;
@@ -226,7 +231,7 @@ __device__ void q_insert32(const Env& E, Trace& T, Key key, bool valid) {
     T.nB += __popc(bm);
     unsigned fm = __ballot_sync(FULL, toF);
     int nI = __popc(fm);
-    if (nI == 0) return;
+    if (nI == 0) return make_int2(T.nF, T.nB);
     // rank of each insert among inserts
     int ii = __popc(fm & lt);
     if (toF) sm->X[ii] = key;
@@ -278,6 +283,7 @@ __device__ void q_insert32(const Env& E, Trace& T, Key key, bool valid) {
     } else {
         T.nF = total;
     }
+    return make_int2(T.nF, T.nB);
 }
 
 // Remove FRONT entries flagged in `rm` (bit i = FRONT[i]).
@@ -317,10 +323,10 @@ __device__ __forceinline__ Key bitonic32(Key x, int lane, bool asc) {
 }
 
 // Move the 32 smallest BACK keys (or all of them) behind the FRONT.
-__device__ void refill(const Env& E, Trace& T) {
-    const KArgs& A = *E.A;
-    WarpSmem* sm = E.sm;
-    const int lane = E.lane;
+__device__ __noinline__ int2 refill(const KArgs* Ap, WarpSmem* sm, long long off, int nF, int nB) {
+    const KArgs& A = *Ap;
+    const int lane = threadIdx.x & 31;
+    QState T{off, nF, nB};
     Key S = kinf();  // running top-32, ascending across lanes
     for (int base = 0; base < T.nB; base += 32) {
         int i = base + lane;
@@ -359,6 +365,7 @@ __device__ void refill(const Env& E, Trace& T) {
         __syncwarp();
     }
     T.nB = w;
+    return make_int2(T.nF, T.nB);
 }
 
 // ---- logging ---------------------------------------------------------------
@@ -370,7 +377,6 @@ struct Round {
     unsigned G;                // granted batch positions
     unsigned evmask;           // positions evicted with a recorded decision
     int ndec;                  // recorded decisions this round
-    unsigned long long dpend;  // digest terms of the current eviction call (lane 0)
     unsigned long long rmF;    // FRONT entries to drop at the rebuild
 };
 
@@ -521,12 +527,12 @@ SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot,
         }
         if (A.P.flags & SS_FLAG_DIGEST) {
             unsigned long long r = (unsigned long long)T.rounds;
-            R.dpend += ss_term(r, SS_TAG_EV0, d, (unsigned long long)v | ((unsigned long long)action << 32));
-            R.dpend += ss_term(r, SS_TAG_EV1, d,
+            c.dpend += ss_term(r, SS_TAG_EV0, d, (unsigned long long)v | ((unsigned long long)action << 32));
+            c.dpend += ss_term(r, SS_TAG_EV1, d,
                                (unsigned long long)(uint32_t)saved | ((unsigned long long)(uint32_t)discarded << 32));
-            R.dpend += ss_term(r, SS_TAG_EV2, d, (unsigned long long)freed);
-            R.dpend += ss_term(r, SS_TAG_EV3, d, dbits(ftb));
-            R.dpend += ss_term(r, SS_TAG_EV4, d, dbits(fta));
+            c.dpend += ss_term(r, SS_TAG_EV2, d, (unsigned long long)freed);
+            c.dpend += ss_term(r, SS_TAG_EV3, d, dbits(ftb));
+            c.dpend += ss_term(r, SS_TAG_EV4, d, dbits(fta));
         }
         c.s_victims += 1;
     }
@@ -563,7 +569,7 @@ __device__ __forceinline__ MemQ mem_q(const MemS& m) {
 // the kernel
 // --------------------------------------------------------------------------
 template <int POL>
-__global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs args) {
+__global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_constant__ KArgs args) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const KArgs& A = args;
     const int lane = threadIdx.x & 31;
@@ -575,8 +581,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
     const int b = A.P.batch_size;
     const long long cap = A.P.memory_capacity;
     const unsigned lt = lanemask_lt();
-    const bool want_digest = (A.P.flags & SS_FLAG_DIGEST) != 0;
-    const bool logging = (A.P.flags & SS_FLAG_ROUND_LOG) && A.out.round_log && A.out.log_offsets;
+#define want_digest ((A.P.flags & SS_FLAG_DIGEST) != 0u)
+#define logging ((A.P.flags & SS_FLAG_ROUND_LOG) != 0u)
 
     for (;;) {
         int t = 0;
@@ -667,7 +673,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                         const uint32_t w = STA(A)[g].w;
                         k = make_key<POL>(w >> 24, DYN(A)[g].ft, w & SLOT_MASK, s, false);
                     }
-                    q_insert32<POL>(E, T, k, mine);
+                    const int2 qs = q_insert32(&A, sm, T.off, T.nF, T.nB, k, mine);
+                    T.nF = qs.x;
+                    T.nB = qs.y;
                     T.cursor += cnt;
                     if (cnt < 32) break;
                 }
@@ -679,7 +687,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                 T.clock = T.next_ready;
                 continue;
             }
-            if (T.nF < b && T.nB > 0) refill(E, T);
+            if (T.nF < b && T.nB > 0) {
+                const int2 qs = refill(&A, sm, T.off, T.nF, T.nB);
+                T.nF = qs.x;
+                T.nB = qs.y;
+            }
             if (lane == 0) c.s_pool += live;
 
             // ---- stage-aware composition (batching.py:46-88)
@@ -767,7 +779,6 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
             R.G = 0;
             R.evmask = 0;
             R.ndec = 0;
-            R.dpend = 0ull;
             R.rmF = (unsigned long long)__ballot_sync(FULL, c_sel);
             // batch members -> M[rank]; the common decode round (batch == ongoing
             // in order) reads its records straight from OM
@@ -890,7 +901,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                         const long long demand = dem_k + reserved;
                         const int d0 = R.ndec;
                         unsigned vcall = 0;
-                        R.dpend = 0ull;
+                        if (lane == 0) c.dpend = 0ull;
+                        __syncwarp();
                         bool ok = true;
                         while (demand + T.used > cap) {
                             if (!evict_one<POL>(E, T, R, slot_k, m, mem, vcall)) {
@@ -943,7 +955,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                         }
                         // success: commit this call's decisions
                         R.evmask |= vcall;
-                        if (lane == 0) dig += R.dpend;
+                        if (lane == 0) dig += c.dpend;
                         if (flg_k & F_Q) {
                             // granted while it still has a heap entry (a victim whose
                             // decision was lost): the reference keeps that stale entry
@@ -1272,7 +1284,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const KArgs ar
                         *fp = *fp & ~F_INS;
                     }
                 }
-                q_insert32<POL>(E, T, k, v);
+                const int2 qs = q_insert32(&A, sm, T.off, T.nF, T.nB, k, v);
+                T.nF = qs.x;
+                T.nB = qs.y;
             }
             T.nins = 0;
         }
