@@ -568,7 +568,9 @@ __device__ __forceinline__ MemQ mem_q(const MemS& m) {
 // --------------------------------------------------------------------------
 // the kernel
 // --------------------------------------------------------------------------
-template <int POL>
+// MODE bit 0: schedule digest, bit 1: per-round log (compile-time so the
+// common configuration carries no branches for the features it does not use)
+template <int POL, int MODE>
 __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_constant__ KArgs args) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const KArgs& A = args;
@@ -581,8 +583,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
     const int b = A.P.batch_size;
     const long long cap = A.P.memory_capacity;
     const unsigned lt = lanemask_lt();
-#define want_digest ((A.P.flags & SS_FLAG_DIGEST) != 0u)
-#define logging ((A.P.flags & SS_FLAG_ROUND_LOG) != 0u)
+    constexpr bool want_digest = (MODE & 1) != 0;
+    constexpr bool logging = (MODE & 2) != 0;
 
     for (;;) {
         int t = 0;
@@ -600,7 +602,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         T.status = SS_TRACE_OK;
         bool anom = false;  // a stale heap entry may exist: general (exact) round path
         if (lane == 0) {
-            c.evictions = c.peak = c.s_pool = c.s_granted = c.s_victims = c.s_res = 0;
+            c.evictions = c.s_pool = c.s_granted = c.s_victims = c.s_res = 0;
             c.logpos = 0;
             c.log = nullptr;
             c.logcap = 0;
@@ -612,6 +614,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             c.n = n;
         }
         unsigned long long dig = 0ull;
+        long long peak = 0;
 
         // ---- init (engine.py:183-199): records, f_t, pre-filter, pending list
         T.npend = 0;
@@ -712,7 +715,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             // in the reference: equal keys are copies of the same request)
             Key pmin = kinf();
             if (!anom) {
-                if (T.nO > 0) pmin = kshfl(okey, 0);
+                if (T.nO > 0) pmin = sm->X[32];
                 if (nc > 0 && klt(sm->F[0], pmin)) pmin = sm->F[0];
             } else {
                 pmin = has_o ? okey : kinf();
@@ -732,8 +735,6 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 // both lists sorted: rank = own index + lower_bound in the other
                 cnt_o = lane;
                 if (cmask) {
-                    if (has_o) sm->X[32 + lane] = okey;
-                    __syncwarp();
                     if (c_elig) {
                         int lo = 0, hi = T.nO;
                         while (lo < hi) {
@@ -991,7 +992,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     dig += ss_term(r64, SS_TAG_TIME, 0, dbits(T.clock));
                 }
                 if (R.ndec > 0 && lane == 0) {
-                    if (T.used > c.peak) c.peak = T.used;
+                    if (T.used > peak) peak = T.used;
                     if (c.log) {
                         const unsigned long long mu = (unsigned long long)T.used, tb = dbits(T.clock);
                         log_put(c, c.logpos + 0, SS_KIND_NONE);
@@ -1200,11 +1201,18 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 const int nc_done = __popc(cdone);
                 const int gi = __popc(R.G & lt), ci = __popc(cdone & lt);
                 if (want_digest) {
-                    if (g_act) dig += ss_term(r64, SS_TAG_GRANT, gi, mem.slot);
-                    if (done) dig += ss_term(r64, SS_TAG_DONE, ci, mem.slot);
-                    if (lane == 31) dig += ss_term(r64, SS_TAG_HDR, 0, ss_hdr_word(kind, ng, nc_done, R.ndec));
-                    if (lane == 30) dig += ss_term(r64, SS_TAG_MEM, 0, (unsigned long long)T.used);
-                    if (lane == 29) dig += ss_term(r64, SS_TAG_TIME, 0, dbits(end));
+                    // one hash stream: granted lanes hash their slot, lanes 29..31
+                    // the round header (a second pass only when they are granted)
+                    const bool hl = lane >= 29;
+                    const uint32_t htag = lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME);
+                    const unsigned long long hval =
+                        lane == 31 ? ss_hdr_word(kind, ng, nc_done, R.ndec)
+                                   : (lane == 30 ? (unsigned long long)T.used : dbits(end));
+                    if (g_act || hl) {
+                        dig += g_act ? ss_term(r64, SS_TAG_GRANT, gi, mem.slot) : ss_term(r64, htag, 0, hval);
+                    }
+                    if (m > 29 && hl && g_act) dig += ss_term(r64, htag, 0, hval);
+                    if (cdone && done) dig += ss_term(r64, SS_TAG_DONE, ci, mem.slot);
                 }
                 if (logging) {
                     const long long lp = c.logpos;
@@ -1225,7 +1233,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         c.logpos = base + ng + nc_done;
                     }
                 }
-                if (lane == 0 && T.used > c.peak) c.peak = T.used;
+                if (T.used > peak) peak = T.used;
                 T.clock = end;
                 T.rounds += 1;
                 // ---- ongoing = granted copies not completed, in granted order
@@ -1241,24 +1249,25 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 } else if (lane < T.nO) {
                     okey = mem_key<POL>(sm->OM[lane]);
                 }
+                // keys mirrored to X[32..] (p* and ranking read them from smem);
                 // keep the ongoing records sorted by their new keys (usually they are)
-                {
-                    const Key nk = kshfl_down(okey, 1);
-                    if (__ballot_sync(FULL, lane + 1 < T.nO && klt(nk, okey))) {
-                        if (lane < T.nO) sm->X[32 + lane] = okey;
-                        __syncwarp();
-                        int r = 0;
-                        for (int k = 0; k < T.nO; k++) {
-                            const Key x = sm->X[32 + k];
-                            if (klt(x, okey) || (keq(x, okey) && k < lane)) r++;
-                        }
-                        MemS mine;
-                        if (lane < T.nO) mine = sm->OM[lane];
-                        __syncwarp();
-                        if (lane < T.nO) sm->OM[r] = mine;
-                        __syncwarp();
-                        if (lane < T.nO) okey = mem_key<POL>(sm->OM[lane]);
+                if (lane < T.nO) sm->X[32 + lane] = okey;
+                __syncwarp();
+                if (__ballot_sync(FULL, lane + 1 < T.nO && klt(sm->X[32 + ((lane + 1) & 31)], okey))) {
+                    int r = 0;
+                    for (int k = 0; k < T.nO; k++) {
+                        const Key x = sm->X[32 + k];
+                        if (klt(x, okey) || (keq(x, okey) && k < lane)) r++;
                     }
+                    MemS mine;
+                    if (lane < T.nO) mine = sm->OM[lane];
+                    __syncwarp();
+                    if (lane < T.nO) {
+                        sm->OM[r] = mine;
+                        sm->X[32 + r] = okey;
+                    }
+                    __syncwarp();
+                    if (lane < T.nO) okey = sm->X[32 + lane];
                 }
             }
             if (logging) {
@@ -1343,7 +1352,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 st->digest = want_digest ? dig : 0ull;
                 st->rounds = T.rounds;
                 st->evictions = c.evictions;
-                st->mem_used_peak = c.peak;
+                st->mem_used_peak = peak;
                 st->log_words = c.log ? (c.logpos < c.logcap ? c.logpos : c.logcap) : 0;
                 st->unservable = c.nuns;
                 st->status = T.status;
@@ -1387,12 +1396,23 @@ void carve_work(void* base, int64_t n, Work* w) {
 
 int sched_smem_bytes() { return (int)(sizeof(WarpSmem) * WPB); }
 
-template <int POL>
-static const void* kernel_ptr() { return (const void*)sched_kernel<POL>; }
+static int mode_of(uint32_t flags) {
+    return ((flags & SS_FLAG_DIGEST) ? 1 : 0) | ((flags & SS_FLAG_ROUND_LOG) ? 2 : 0);
+}
 
-static const void* kernel_for(int policy) {
+template <int POL>
+static const void* kernel_ptr(int mode) {
+    switch (mode) {
+    case 0: return (const void*)sched_kernel<POL, 0>;
+    case 1: return (const void*)sched_kernel<POL, 1>;
+    case 2: return (const void*)sched_kernel<POL, 2>;
+    default: return (const void*)sched_kernel<POL, 3>;
+    }
+}
+
+static const void* kernel_for(int policy, int mode) {
     switch (policy) {
-    case SS_POLICY_SEMANTIC: return kernel_ptr<SS_POLICY_SEMANTIC>();
+    case SS_POLICY_SEMANTIC: return kernel_ptr<SS_POLICY_SEMANTIC>(mode);
     default: return nullptr;
     }
 }
@@ -1401,7 +1421,7 @@ int sched_max_blocks(int policy, int* sm_count) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const void* k = kernel_for(policy);
+    const void* k = kernel_for(policy, 1);
     if (!k) return 0;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sched_smem_bytes());
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, 32 * WPB, sched_smem_bytes());
@@ -1412,13 +1432,10 @@ int sched_max_blocks(int policy, int* sm_count) {
 int launch_sched(const KArgs& a, int blocks, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     size_t smem = (size_t)sched_smem_bytes();
-    switch (a.P.policy) {
-    case SS_POLICY_SEMANTIC:
-        sched_kernel<SS_POLICY_SEMANTIC><<<blocks, 32 * WPB, smem, st>>>(a);
-        break;
-    default:
-        return SS_ERR_UNSUPPORTED;
-    }
+    const void* k = kernel_for(a.P.policy, mode_of(a.P.flags));
+    if (!k) return SS_ERR_UNSUPPORTED;
+    void* argv[] = {(void*)&a};
+    if (cudaLaunchKernel(k, dim3(blocks), dim3(32 * WPB), argv, smem, st) != cudaSuccess) return SS_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? SS_OK : SS_ERR_CUDA;
 }
 
