@@ -38,7 +38,7 @@ int validate(const ss_params* p, const ss_trace_batch* b, const ss_outputs* o) {
     if (p->decode_cost_sum != 0 && p->decode_cost_sum != 1)
         return fail(SS_ERR_INVALID_ARG, "decode_batch_cost must be 'max' or 'sum'");
     if (p->batch_size > SS_MAX_BATCH) return fail(SS_ERR_UNSUPPORTED, "batch size above SS_MAX_BATCH (32)");
-    if (p->policy != SS_POLICY_SEMANTIC) return fail(SS_ERR_UNSUPPORTED, "policy not implemented on the device");
+    if (p->policy < SS_POLICY_SEMANTIC || p->policy > SS_POLICY_HPJF) return fail(SS_ERR_INVALID_ARG, "unknown policy");
     if (b->n_traces < 0 || b->n_requests < 0) return fail(SS_ERR_INVALID_ARG, "negative sizes");
     if (b->n_traces > 0 && (!b->trace_offsets)) return fail(SS_ERR_INVALID_ARG, "trace_offsets is null");
     if (b->n_requests > 0 &&

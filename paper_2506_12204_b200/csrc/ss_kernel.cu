@@ -698,7 +698,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             if (lane == 0) c.s_pool += live;
 
             // ---- stage-aware composition (batching.py:46-88)
-            const int nc = T.nF < b ? T.nF : b;
+            // candidates popped from the queue: top-b (semantic / SJF / HPJF,
+            // batching.py:46-54, engine.py:270-276) or the b - |ongoing| that FCFS
+            // adds behind its non-preemptible ongoing members (engine.py:256-262)
+            const int cwant = POL == SS_POLICY_FCFS ? b - T.nO : b;
+            const int nc = T.nF < cwant ? T.nF : cwant;
             const bool has_c = lane < nc;
             const bool has_o = lane < T.nO;
             Key ck;  // candidate key: stored (fast path) or current (general path)
@@ -714,7 +718,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             // copies are sorted by key across lanes (their order is unobservable
             // in the reference: equal keys are copies of the same request)
             Key pmin = kinf();
-            if (!anom) {
+            if (POL != SS_POLICY_SEMANTIC) {
+            } else if (!anom) {
                 if (T.nO > 0) pmin = sm->X[32];
                 if (nc > 0 && klt(sm->F[0], pmin)) pmin = sm->F[0];
             } else {
@@ -726,12 +731,19 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     if (klt(x, pmin)) pmin = x;
                 }
             }
+            // semantic: the stage of p* decides which candidates are eligible;
+            // the baselines take every candidate (no stage awareness)
             const bool pstar_prefill = !(pmin.aux & DEC_BIT);
-            const int kind = pstar_prefill ? SS_KIND_PREFILL : SS_KIND_DECODE;
-            const bool c_elig = has_c && (pstar_prefill || (ck.aux & DEC_BIT));
+            int kind = pstar_prefill ? SS_KIND_PREFILL : SS_KIND_DECODE;
+            const bool c_elig =
+                has_c && (POL != SS_POLICY_SEMANTIC || pstar_prefill || (ck.aux & DEC_BIT));
             const unsigned cmask = __ballot_sync(FULL, c_elig);
             int cnt_c = 0, cnt_o = 0;
-            if (!anom) {
+            if (POL == SS_POLICY_FCFS) {
+                // ongoing first in their order, then the popped candidates
+                cnt_o = lane;
+                cnt_c = T.nO + lane;
+            } else if (!anom) {
                 // both lists sorted: rank = own index + lower_bound in the other
                 cnt_o = lane;
                 if (cmask) {
@@ -844,6 +856,10 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             if (act) {
                 mem = direct ? sm->OM[lane] : sm->M[lane];
                 if (anom) mem.flg = *FLG(A, T.off + mem.slot);  // queued bit may have moved
+            }
+            if (POL != SS_POLICY_SEMANTIC) {
+                // BatchKind from the selected members' stages (engine.py:263-267, 280-284)
+                kind = __ballot_sync(FULL, act && (mem.flg & F_STAGE) != ST_DEC) ? SS_KIND_PREFILL : SS_KIND_DECODE;
             }
             const int nO_start = T.nO;
             const int nuns_start = c.nuns;
@@ -1253,7 +1269,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 // keep the ongoing records sorted by their new keys (usually they are)
                 if (lane < T.nO) sm->X[32 + lane] = okey;
                 __syncwarp();
-                if (__ballot_sync(FULL, lane + 1 < T.nO && klt(sm->X[32 + ((lane + 1) & 31)], okey))) {
+                if (POL != SS_POLICY_FCFS &&
+                    __ballot_sync(FULL, lane + 1 < T.nO && klt(sm->X[32 + ((lane + 1) & 31)], okey))) {
                     int r = 0;
                     for (int k = 0; k < T.nO; k++) {
                         const Key x = sm->X[32 + k];
@@ -1413,6 +1430,9 @@ static const void* kernel_ptr(int mode) {
 static const void* kernel_for(int policy, int mode) {
     switch (policy) {
     case SS_POLICY_SEMANTIC: return kernel_ptr<SS_POLICY_SEMANTIC>(mode);
+    case SS_POLICY_FCFS: return kernel_ptr<SS_POLICY_FCFS>(mode);
+    case SS_POLICY_SJF: return kernel_ptr<SS_POLICY_SJF>(mode);
+    case SS_POLICY_HPJF: return kernel_ptr<SS_POLICY_HPJF>(mode);
     default: return nullptr;
     }
 }

@@ -13,8 +13,8 @@ from paper_2506_12204_b200 import _abi as A
 
 pytestmark = pytest.mark.gpu
 
-SMALL = [c for c in golden_cases("small") if c["params"]["policy"] == "semantic"]
-LARGE = [c for c in golden_cases("large") if c["params"]["policy"] == "semantic"]
+SMALL = golden_cases("small")
+LARGE = golden_cases("large")
 ANOM = golden_cases("anomaly")
 
 
@@ -96,6 +96,22 @@ def test_gpu_many_traces_vs_oracle(native, capacity):
     gpu = native.run_host(p(), batch)
     cpu = run_oracle(p(), batch, threads=8)
     assert _compare_with_oracle(gpu, cpu, batch) >= batch.n_traces // 2
+
+
+@pytest.mark.parametrize("policy", ["fcfs", "sjf", "hpjf"])
+@pytest.mark.parametrize("capacity", [10**9, 900])
+def test_gpu_baseline_policies_vs_oracle(native, policy, capacity):
+    """FCFS / SJF / HPJF (engine.py:114-123, 256-285), including eviction by
+    each policy's key, against the oracle on many traces."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.results import make_params
+
+    batch, cfg = _seeded_batch(48, 250, dict(levels=3), seed0=500)
+    for b in (1, 5, 16):
+        p = lambda: make_params(cfg.gpu_profile(), b, capacity, policy=policy, levels=3, flags=A.SS_FLAG_DIGEST)
+        gpu = native.run_host(p(), batch)
+        cpu = run_oracle(p(), batch, threads=8)
+        _compare_with_oracle(gpu, cpu, batch)
 
 
 @pytest.mark.parametrize("prof", ["a100_qwen7b", "a5000_qwen7b", "mixed"])
