@@ -94,7 +94,9 @@ typedef struct ss_params {
     int32_t decode_cost_sum;   /* 0: "max", 1: "sum"   (engine.py:148)        */
     int32_t levels;            /* true-urgency levels for the stats (<=16)    */
     uint32_t flags;            /* SS_FLAG_*                                    */
-    int64_t max_rounds;        /* per-trace round cap, 0 = unlimited          */
+    int64_t max_rounds;        /* per-trace round cap; 0 = automatic:
+                                  64 * (requests + sum of true output lengths)
+                                  + 100000, far above any progressing schedule */
 } ss_params;
 
 /* Requests of all traces, concatenated; trace t owns

@@ -674,6 +674,12 @@ static void run_trace(const ss_params* P, const ss_trace_batch* B, const int64_t
     int next = 0;
     s->clock = 0.0;
     int64_t max_rounds = P->max_rounds;
+    if (max_rounds <= 0) {                 /* same automatic cap as the device */
+        int64_t tokens = 0;
+        for (int i = 0; i < n; i++) tokens += s->r[i].true_out;
+        max_rounds = 64 * (tokens + n) + 100000;
+    }
+    if (max_rounds > 0x7fffffffll) max_rounds = 0x7fffffffll;
     for (;;) {                                                       /* engine.py:202-224 */
         while (next < npend && s->r[pending[next]].ready <= s->clock + 1e-12) {
             s->buffer[s->nbuf++] = pending[next]; s->r[pending[next]].in_buffer = 1; next++;
@@ -704,7 +710,7 @@ static void run_trace(const ss_params* P, const ss_trace_batch* B, const int64_t
             s->status = SS_TRACE_LIVELOCK;
             break;
         }
-        if (max_rounds > 0 && s->rounds >= max_rounds) { s->status = SS_TRACE_ROUND_CAP; break; }
+        if (s->rounds >= max_rounds) { s->status = SS_TRACE_ROUND_CAP; break; }
     }
     free(pending);
     if (s->log_overflow && !s->status) s->status = SS_TRACE_LOG_OVERFLOW;

@@ -619,6 +619,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         // ---- init (engine.py:183-199): records, f_t, pre-filter, pending list
         T.npend = 0;
         int nuns = 0;
+        long long tokens = 0;
         for (int base = 0; base < n; base += 32) {
             int i = base + lane;
             bool v = i < n;
@@ -629,6 +630,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 uint4 st;
                 st.x = prompt;
                 st.y = A.in.true_output_len[g];
+                tokens += st.y;
                 st.z = mid;
                 st.w = ((uint32_t)A.in.pred_urgency[g] << 24) | A.in.tie_rank[g];
                 STA(A)[g] = st;
@@ -645,6 +647,15 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             nuns += __popc(um);
         }
         if (lane == 0) c.nuns = nuns;
+        // round cap: params.max_rounds, or automatic (the reference has no guard
+        // and can cycle forever under some tight-memory schedules)
+        tokens += __shfl_xor_sync(FULL, tokens, 16);
+        tokens += __shfl_xor_sync(FULL, tokens, 8);
+        tokens += __shfl_xor_sync(FULL, tokens, 4);
+        tokens += __shfl_xor_sync(FULL, tokens, 2);
+        tokens += __shfl_xor_sync(FULL, tokens, 1);
+        long long round_cap = A.P.max_rounds > 0 ? A.P.max_rounds : 64 * (tokens + n) + 100000;
+        if (round_cap > 0x7fffffffll) round_cap = 0x7fffffffll;
         T.cursor = 0;
         __syncwarp();
         T.next_ready = T.npend > 0 ? A.in.ready_time[T.off + A.w.pend[T.off]] : INFINITY;
@@ -1291,7 +1302,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 __syncwarp();
                 if (c.logpos > c.logcap) set_status(T, SS_TRACE_LOG_OVERFLOW);
             }
-            if (A.P.max_rounds > 0 && T.rounds >= A.P.max_rounds) set_status(T, SS_TRACE_ROUND_CAP);
+            if (T.rounds >= round_cap) set_status(T, SS_TRACE_ROUND_CAP);
 
             // ---- queue rebuild: drop popped FRONT entries, then insert this
             //      round's pushed-back / failed / evicted requests with the key
