@@ -207,6 +207,14 @@ __device__ __forceinline__ void store_dyn(const KArgs& A, long long g, double ft
     DYN(A)[g] = d;
 }
 __device__ __forceinline__ uint32_t* FLG(const KArgs& A, long long g) { return &DYN(A)[g].flg; }
+// read-modify-write of a request's flags in HBM (copies of one request in other
+// lanes may hold stale register values, so never write a lane's copy back)
+__device__ __forceinline__ uint32_t flg_update(const KArgs& A, long long g, uint32_t clear, uint32_t set) {
+    uint32_t* fp = FLG(A, g);
+    const uint32_t f = (*fp & ~clear) | set;
+    *fp = f;
+    return f;
+}
 
 // ---- queue front / back maintenance --------------------------------------
 
@@ -811,8 +819,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             if (c_sel) {
                 MemS cm;
                 load_mem(A, T.off, ck.aux & SLOT_MASK, cm);
-                cm.flg &= ~F_Q;  // popped from the heap for good
-                *FLG(A, T.off + cm.slot) = cm.flg;
+                cm.flg = flg_update(A, T.off + cm.slot, F_Q, 0u);  // popped from the heap for good
                 sm->M[cnt_c] = cm;
             }
             if (!direct && has_o && cnt_o < m) sm->M[cnt_o] = sm->OM[lane];
@@ -912,11 +919,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     if (lane == 0) c.s_res += T.nR;
                     // slow path: one member at a time from the first that must evict
                     long long reserved = __shfl_sync(FULL, excl, f);
-                    if ((R.G >> lane) & 1u) {
-                        mem.flg |= F_GRANT;
-                        *FLG(A, T.off + mem.slot) = mem.flg;
-                    }
+                    if ((R.G >> lane) & 1u) flg_update(A, T.off + mem.slot, 0u, F_GRANT);
                     __syncwarp();
+                    if (act) mem.flg = *FLG(A, T.off + mem.slot);
                     for (int k = f; k < m && T.status == SS_TRACE_OK; k++) {
                         if ((R.evmask >> k) & 1u) continue;
                         q = mem_q(mem);
@@ -957,26 +962,24 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                         A.w.R[T.off + ri] = last;
                                         A.w.rpos[T.off + last] = ri;
                                     }
-                                    mem.flg = (mem.flg & ~(F_STAGE | F_Q | F_INS | F_GRANT)) | ST_UNS;
-                                    *FLG(A, g) = mem.flg;
+                                    flg_update(A, g, F_STAGE | F_Q | F_INS | F_GRANT, ST_UNS);
                                     A.out.unservable_slots[T.off + un] = mem.slot;
                                     c.nuns = un + 1;
                                 }
                                 if (isdec_k) T.nR -= 1;
                                 T.used -= kvd_k;
                                 __syncwarp();
-                                // other batch copies of it see the new state
-                                if (lane != k && act && mem.slot == slot_k) mem.flg = *FLG(A, T.off + slot_k);
+                                // every batch copy of it sees the new state
+                                if (act && mem.slot == slot_k) mem.flg = *FLG(A, T.off + slot_k);
                             } else if (!(flg_k & F_Q)) {
                                 if (lane == k) {
                                     const Key kk = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, q.isdec);
-                                    mem.flg |= F_Q | F_INS;
-                                    *FLG(A, T.off + mem.slot) = mem.flg;
+                                    flg_update(A, T.off + mem.slot, 0u, F_Q | F_INS);
                                     INS(A)[T.off + T.nins] = kk;
                                 }
                                 T.nins += 1;
                                 __syncwarp();
-                                if (lane != k && act && mem.slot == slot_k) mem.flg = *FLG(A, T.off + slot_k);
+                                if (act && mem.slot == slot_k) mem.flg = *FLG(A, T.off + slot_k);
                             }
                             __syncwarp();
                             continue;
@@ -992,16 +995,23 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         }
                         R.G |= 1u << k;
                         reserved += imm_k;
-                        if (lane == k) {
-                            mem.flg |= F_GRANT;
-                            *FLG(A, T.off + mem.slot) = mem.flg;
-                        }
+                        if (lane == k) flg_update(A, T.off + mem.slot, 0u, F_GRANT);
                         __syncwarp();
-                        if (act && lane != k && mem.slot == slot_k) mem.flg |= F_GRANT;
+                        if (act && mem.slot == slot_k) mem.flg = *FLG(A, T.off + slot_k);
                     }
                 }
             }
             if (T.status != SS_TRACE_OK) break;
+            if (anom) {
+                // copies of one request must agree before duration and execution
+                __syncwarp();
+                if (act) {
+                    const Dyn d = DYN(A)[T.off + mem.slot];
+                    mem.ft = d.ft;
+                    mem.dec = d.dec;
+                    mem.flg = d.flg;
+                }
+            }
             const bool g_act = (R.G >> lane) & 1u;
             const int ng = __popc(R.G);
             const unsigned long long r64 = (unsigned long long)T.rounds;
@@ -1115,7 +1125,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     }
                     // allocations all fit (admission reserved them); completions release
                     T.used += (long long)__reduce_add_sync(FULL, delta);
-                    if (T.used > cap || T.used < 0) set_status(T, SS_TRACE_INTERNAL);
+                    if (T.used > cap) set_status(T, SS_TRACE_REF_ERROR);  // mem.allocate raises
+                    if (T.used < 0) set_status(T, SS_TRACE_INTERNAL);
                     const unsigned nmr = __ballot_sync(FULL, newres);
                     if (nmr) {
                         if (newres) {
