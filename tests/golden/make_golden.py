@@ -398,6 +398,12 @@ def cases_anomaly():
         for sd in seeds:
             c = scen(workload=WorkloadSpec(total_requests=300, seed=sd, levels=3), seed=sd, memory_capacity=cap)
             out.append((f"anom_c{cap}_s{sd}", c, gen_arrivals(c), sd < 4))
+    # baseline policies evicting by their own keys under the same pressure
+    for pol in (Policy.FCFS, Policy.SJF, Policy.HPJF):
+        for b, sd in ((16, 500), (5, 501), (16, 522), (16, 529)):
+            c = scen(policy=pol, batch_size=b, workload=WorkloadSpec(total_requests=250, seed=sd, levels=3),
+                     seed=sd, memory_capacity=900)
+            out.append((f"anom_{pol.value}_b{b}_s{sd}", c, gen_arrivals(c), sd == 500))
     return out
 
 
