@@ -42,6 +42,10 @@ WORKLOADS = {
     "E": dict(desc="config E: 65,536 traces x 2,000 requests per job (generate(WorkloadSpec(total_requests=2000, "
                    "seed=s))), b=16, ample KV, a100_qwen7b",
               traces=65536, requests=2000, capacity=10**9, profile="a100_qwen7b", levels=5),
+    "C": dict(desc="config C: one pool of 1,000,000 requests all at t=0 (WorkloadSpec(total_requests=N, "
+                   "concurrent=N, concurrent_mode='fixed', seed=1)), b=16, ample KV, a100_qwen7b; steady-state "
+                   "per-step time from runs capped at 1 and 1+S rounds",
+              traces=1, requests=1_000_000, capacity=10**9, profile="a100_qwen7b", levels=5),
     "D": dict(desc="config D shape at scale: 4,096 traces x 1,000 requests, 3 levels, KV budget 2,295 slots "
                    "(25% of the seed-1 ample peak), a100_qwen7b (offload), heavy eviction",
               traces=4096, requests=1000, capacity=2295, profile="a100_qwen7b", levels=3),
@@ -173,6 +177,84 @@ def reference_arm(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def pool_bench(args, wl):
+    """Config C: per-step latency of one million-request pool (replicas only)."""
+    from paper_2506_12204_b200 import _abi as A
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.results import make_params
+    from paper_2506_12204_b200.tracegen import generate_batch
+    from paper_2506_12204_b200.workload import WorkloadSpec
+
+    N = args.traces or wl["requests"]
+    spec = WorkloadSpec(total_requests=N, concurrent=N, concurrent_mode="fixed", seed=1)
+    S = args.pool_steps
+    prof = get_profile(wl["profile"])
+    pf = lambda cap_rounds: make_params(prof, 16, wl["capacity"], levels=5, flags=A.SS_FLAG_DIGEST,
+                                        max_rounds=cap_rounds)
+    if args.impl == "reference":
+        batch = generate_batch(spec, [1], pinned=False)
+        from oracle_binding import run_oracle
+
+        S = 10 * S  # the port's per-step cost is small next to its 1M-request setup
+        t = {}
+        for r in (1, 1 + S):
+            ts = []
+            for _ in range(max(1, args.steps)):
+                t0 = time.perf_counter()
+                run_oracle(pf(r), batch)
+                ts.append(time.perf_counter() - t0)
+            t[r] = min(ts)
+        per = (t[1 + S] - t[1]) / S
+        line = {"metric": "scheduler decisions/sec (one 1M-request pool, steady state)", "value": 1.0 / per,
+                "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "replicas only",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": {"workload": wl["desc"], "pool_steps": S, "first_step_s": t[1]},
+                "cpu_baseline": {"value": 1.0 / per, "unit": UNIT, "cores": 1, "kind": "port",
+                                 "sample": f"{S} steady-state steps of the 1M pool, oracle port, 1 thread"},
+                "e2e": {"value": 1.0 / per, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    import torch
+    from paper_2506_12204_b200 import native
+
+    batch = generate_batch(spec, [1], pinned=True)
+    dev = torch.device("cuda", 0)
+    dbatch = native.DeviceBatch(batch, dev)
+    douts = native.DeviceOutputs(batch.n_requests, 1, dev, with_state=False)
+    ws = native.Workspace(pf(1), 1, batch.n_requests, dev)
+    for _ in range(args.warmup):
+        native.run_device(pf(1 + S), dbatch, douts, ws, time_kernel=True)
+    t = {}
+    for r in (1, 1 + S):
+        t[r] = min(native.run_device(pf(r), dbatch, douts, ws, time_kernel=True) for _ in range(max(1, args.steps)))
+    per_ms = (t[1 + S] - t[1]) / S
+    st = douts.stats_numpy()
+    line = {"metric": "scheduler decisions/sec (one 1M-request pool, steady state)", "value": 1e3 / per_ms,
+            "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_ms,
+            "higher_is_better": True, "scaling": "replicas only", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": wl["desc"], "requests": N, "pool_steps": S, "first_step_ms": t[1],
+                       "capped_run_ms": t[1 + S], "rounds_run": int(st["rounds"][0])},
+            "gpu_launches": 1}
+    if not args.no_cpu:
+        from oracle_binding import run_oracle
+
+        tc = {}
+        S2 = 10 * S
+        for r in (1, 1 + S, 1 + S2):
+            t0 = time.perf_counter()
+            res = run_oracle(pf(r), batch)
+            tc[r] = time.perf_counter() - t0
+            if r == 1 + S:
+                match = bool(res.stats["digest"][0] == st["digest"][0] and res.stats["rounds"][0] == st["rounds"][0])
+        line["cpu_baseline"] = {"value": S2 / (tc[1 + S2] - tc[1]), "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"{S2} steady-state steps, oracle port 1 thread, first step "
+                                          f"{tc[1]:.2f} s"}
+        line["parity"] = {"digest_and_rounds_match_after_steps": match}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -183,8 +265,11 @@ def main():
     ap.add_argument("--traces", type=int, default=None, help="override traces per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--pool-steps", type=int, default=20000, help="config C: steady-state steps per sample")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
+    if args.workload == "C":
+        return pool_bench(args, wl)
     if args.impl == "reference":
         return reference_arm(args, wl)
 
