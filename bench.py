@@ -113,8 +113,10 @@ def build_batch(wl, rank, traces_override=None, pinned=True):
     from paper_2506_12204_b200.tracegen import generate_batch
     from paper_2506_12204_b200.workload import WorkloadSpec
 
+    from paper_2506_12204_b200.dist import shard_seeds
+
     T = traces_override or wl["traces"]
-    seeds = np.arange(rank * T, (rank + 1) * T, dtype=np.int64)
+    seeds = shard_seeds(T, rank)
     spec = WorkloadSpec(total_requests=wl["requests"], levels=wl["levels"])
     return generate_batch(spec, seeds, pinned=pinned), T
 
