@@ -97,7 +97,15 @@ typedef struct ss_params {
     int64_t max_rounds;        /* per-trace round cap; 0 = automatic:
                                   64 * (requests + sum of true output lengths)
                                   + 100000, far above any progressing schedule */
+    int64_t bulk_min;          /* bulk admission: a trace whose first round admits
+                                  >= bulk_min requests (config C: 1M at t = 0) gets
+                                  them as one sorted run built by the grid-wide
+                                  radix sort instead of per-warp queue inserts.
+                                  0 = SS_BULK_MIN_DEFAULT, < 0 = never. Results
+                                  are identical either way (tests force 1).      */
 } ss_params;
+
+#define SS_BULK_MIN_DEFAULT 1024
 
 /* Requests of all traces, concatenated; trace t owns
  * [trace_offsets[t], trace_offsets[t+1]), in pending order. */
@@ -247,6 +255,11 @@ int ss_run_traces(const ss_params* params, const ss_trace_batch* batch,
  * reference-facing plugin call (host buffers in, host buffers out). */
 int ss_run_traces_host(const ss_params* params, const ss_trace_batch* batch,
                        const ss_outputs* out, void* stream, float* kernel_ms);
+
+/* Device times of the calling thread's last ss_run_traces made with a
+ * non-NULL kernel_ms: the grid-wide prepass (request init + bulk-admission
+ * radix sort) and the scheduler kernel. */
+int ss_last_timings(float* prepass_ms, float* kernel_ms);
 
 /* Number of warps the scheduler kernel keeps resident (for reporting). */
 int ss_kernel_config(const ss_params* params, int32_t n_traces, int* blocks,

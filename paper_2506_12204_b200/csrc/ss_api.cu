@@ -12,6 +12,7 @@
 namespace {
 
 thread_local std::string g_err;
+thread_local float g_prepass_ms = 0.f, g_kernel_ms = 0.f;
 
 int fail(int code, const char* msg) {
     g_err = msg;
@@ -69,6 +70,12 @@ extern "C" {
 
 const char* ss_last_error(void) { return g_err.c_str(); }
 
+int ss_last_timings(float* prepass_ms, float* kernel_ms) {
+    if (prepass_ms) *prepass_ms = g_prepass_ms;
+    if (kernel_ms) *kernel_ms = g_kernel_ms;
+    return SS_OK;
+}
+
 int ss_device_info(int* device, int* sm_count, int* cc_major, int* cc_minor) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(SS_ERR_NO_DEVICE, "no CUDA device");
@@ -83,9 +90,9 @@ int ss_device_info(int* device, int* sm_count, int* cc_major, int* cc_minor) {
 
 int ss_workspace_bytes(const ss_params* params, int32_t n_traces, int64_t n_requests, size_t* bytes) {
     (void)params;
-    (void)n_traces;
     if (!bytes) return fail(SS_ERR_INVALID_ARG, "null bytes");
-    *bytes = ss::work_bytes(n_requests);
+    if (n_traces < 0 || n_requests < 0) return fail(SS_ERR_INVALID_ARG, "negative sizes");
+    *bytes = ss::work_bytes(n_requests, n_traces);
     return SS_OK;
 }
 
@@ -112,7 +119,7 @@ int ss_run_traces(const ss_params* params, const ss_trace_batch* batch, const ss
         return SS_OK;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    size_t need = ss::work_bytes(batch->n_requests);
+    size_t need = ss::work_bytes(batch->n_requests, batch->n_traces);
     void* ws = workspace;
     bool own = false;
     if (!ws) {
@@ -125,17 +132,24 @@ int ss_run_traces(const ss_params* params, const ss_trace_batch* batch, const ss
     a.P = *params;
     a.in = *batch;
     a.out = *out;
-    ss::carve_work(ws, batch->n_requests, &a.w);
-    CK(cudaMemsetAsync(a.w.next_trace, 0, sizeof(int), st));
+    ss::carve_work(ws, batch->n_requests, batch->n_traces, &a.w);
+    CK(cudaMemsetAsync(ws, 0, ss::work_zero_bytes(batch->n_traces), st));
     int blocks = 0;
     rc = ss_kernel_config(params, batch->n_traces, &blocks, nullptr, nullptr);
     if (rc) return rc;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t e0 = nullptr, em = nullptr, e1 = nullptr;
     if (kernel_ms) {
         CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&em));
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, st));
     }
+    rc = ss::launch_prepass(a, stream);
+    if (rc) {
+        cudaError_t e = cudaGetLastError();
+        return e != cudaSuccess ? cuda_fail(e, "prepass launch") : fail(rc, "prepass launch failed");
+    }
+    if (kernel_ms) CK(cudaEventRecord(em, st));
     rc = ss::launch_sched(a, blocks, stream);
     if (rc) {
         cudaError_t e = cudaGetLastError();
@@ -144,8 +158,11 @@ int ss_run_traces(const ss_params* params, const ss_trace_batch* batch, const ss
     if (kernel_ms) {
         CK(cudaEventRecord(e1, st));
         CK(cudaEventSynchronize(e1));
-        CK(cudaEventElapsedTime(kernel_ms, e0, e1));
+        CK(cudaEventElapsedTime(&g_prepass_ms, e0, em));
+        CK(cudaEventElapsedTime(&g_kernel_ms, em, e1));
+        *kernel_ms = g_kernel_ms;
         cudaEventDestroy(e0);
+        cudaEventDestroy(em);
         cudaEventDestroy(e1);
     }
     if (own) {
@@ -176,7 +193,7 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
     size_t out_b = 2 * a16(nn * 8) + 2 * a16(nn * 4) + a16(nn * 8) + a16(nn * 4) +
                    a16((size_t)T * sizeof(ss_trace_stats)) + a16(nn * 4);
     size_t log_b = logr ? a16((size_t)log_words * 4) + a16((T + 1) * 8) : 0;
-    size_t ws_b = ss::work_bytes(n);
+    size_t ws_b = ss::work_bytes(n, T);
     size_t total = in_b + out_b + log_b + ws_b;
     std::lock_guard<std::mutex> lk(g_stage.mu);
     cudaStream_t st = (cudaStream_t)stream;

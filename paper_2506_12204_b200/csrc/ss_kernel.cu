@@ -7,10 +7,12 @@
 //
 // Per-trace state:
 //   * dispatch queue = sorted FRONT (64 packed keys, shared memory) + unsorted
-//     BACK (HBM); every BACK key is larger than every FRONT key, so the
-//     top-b candidates are FRONT[0..b) and the dual heap of heaps.py:32-237
-//     becomes a merge-by-rank in shared memory. The BACK is refilled with a
-//     warp bitonic top-32 selection when the FRONT runs short.
+//     BACK (HBM) + a sorted RUN (HBM, the bulk admission sorted grid-wide by
+//     ss_prepass.cu, consumed from its front); every BACK / RUN key is larger
+//     than every FRONT key, so the top-b candidates are FRONT[0..b) and the
+//     dual heap of heaps.py:32-237 becomes a merge-by-rank in shared memory.
+//     The FRONT is refilled with a warp bitonic top-32 of the BACK merged with
+//     the next 32 RUN keys when it runs short.
 //   * ongoing batch (engine.py:165): one record per lane, kept sorted by key,
 //     stored in shared memory between rounds (keys stay in registers).
 //   * resident set (the eviction heap, heaps.py:174-207) is an unsorted HBM
@@ -30,6 +32,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "ss_common.cuh"
 #include "ss_costs.cuh"
 #include "ss_kernel.cuh"
 
@@ -44,17 +47,6 @@
 
 namespace ss {
 
-constexpr unsigned FULL = 0xffffffffu;
-constexpr uint32_t ST_WAIT = 0, ST_DEC = 2, ST_DONE = 5, ST_UNS = 6;
-constexpr uint32_t F_STAGE = 7u, F_PF = 8u, F_Q = 16u, F_INS = 32u, F_FIRST = 64u, F_GRANT = 128u;
-constexpr uint32_t SLOT_MASK = 0x00FFFFFFu, DEC_BIT = 0x80000000u;
-
-struct __align__(16) Key {
-    unsigned long long hi;
-    uint32_t lo;
-    uint32_t aux;  // slot | decoding << 31
-};
-
 // a request's state as one unit: static record, dynamic record, slot
 struct __align__(16) MemS {
     uint4 st;      // prompt, true_out, pred_len, rank << 24 | tie
@@ -64,18 +56,14 @@ struct __align__(16) MemS {
     uint32_t slot, _pad0, _pad1, _pad2;
 };
 
-// dynamic record of a request in HBM
-struct __align__(16) Dyn {
-    double ft;
-    uint32_t dec;
-    uint32_t flg;
-};
-
 // trace state touched once per round or less: shared memory, lane 0 writes
 struct Cold {
     long long evictions, peak, s_pool, s_granted, s_victims, s_res, logpos, logcap;
     unsigned long long dpend;  // digest terms of the current eviction call
     uint32_t* log;
+    long long rbase;  // this trace's sorted RUN in w.S starts at rbase + rpos
+    int rpos, bulk;   // RUN cursor; requests admitted in bulk (first round)
+    int dense;        // no unservable request: pending index == slot
     int nuns, lost, anomalies, n;
 };
 
@@ -93,17 +81,6 @@ __device__ __forceinline__ uint32_t m_mid(const MemS& m) { return m.st.z; }
 __device__ __forceinline__ uint32_t m_rank(const MemS& m) { return m.st.w >> 24; }
 __device__ __forceinline__ uint32_t m_tie(const MemS& m) { return m.st.w & SLOT_MASK; }
 
-__device__ __forceinline__ bool klt(const Key& a, const Key& b) {
-    return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo);
-}
-__device__ __forceinline__ bool keq(const Key& a, const Key& b) { return a.hi == b.hi && a.lo == b.lo; }
-__device__ __forceinline__ Key kinf() {
-    Key k;
-    k.hi = ~0ull;
-    k.lo = ~0u;
-    k.aux = ~0u;
-    return k;
-}
 __device__ __forceinline__ Key kshfl(const Key& k, int src) {
     Key r;
     r.hi = __shfl_sync(FULL, k.hi, src);
@@ -137,27 +114,6 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 }
 
 template <int POL>
-__device__ __forceinline__ Key make_key(uint32_t urank, double ft, uint32_t tie, uint32_t slot,
-                                        bool decoding) {
-    unsigned long long fb = (unsigned long long)__double_as_longlong(ft);
-    Key k;
-    if (POL == SS_POLICY_SEMANTIC) {
-        k.hi = ((unsigned long long)urank << 56) | (fb >> 7);
-        k.lo = ((uint32_t)(fb & 127ull) << 25) | tie;
-    } else if (POL == SS_POLICY_FCFS) {
-        k.hi = 0ull;
-        k.lo = tie;
-    } else if (POL == SS_POLICY_SJF) {
-        k.hi = fb >> 7;
-        k.lo = ((uint32_t)(fb & 127ull) << 25) | tie;
-    } else {
-        k.hi = (unsigned long long)urank << 56;
-        k.lo = tie;
-    }
-    k.aux = slot | (decoding ? DEC_BIT : 0u);
-    return k;
-}
-template <int POL>
 __device__ __forceinline__ Key mem_key(const MemS& m) {
     return make_key<POL>(m_rank(m), m.ft, m_tie(m), m.slot, (m.flg & F_STAGE) == ST_DEC);
 }
@@ -181,6 +137,7 @@ struct Trace {
     double next_ready;  // ready time of the next pending request (inf if none)
     int npend, cursor;
     int nF, nB, nR, nO, nins;
+    int nRun;  // keys left in the sorted RUN
     int rounds, status;
 };
 
@@ -223,8 +180,8 @@ struct QState {
     long long off;
     int nF, nB;
 };
-__device__ __noinline__ int2 q_insert32(const KArgs* Ap, WarpSmem* sm, long long off, int nF, int nB, Key key,
-                                        bool valid) {
+__device__ __noinline__ int2 q_insert32(const KArgs* Ap, WarpSmem* sm, long long off, int nF, int nB, int nRun,
+                                        Key key, bool valid) {
     const KArgs& A = *Ap;
     const int lane = threadIdx.x & 31;
     QState T{off, nF, nB};
@@ -232,7 +189,7 @@ __device__ __noinline__ int2 q_insert32(const KArgs* Ap, WarpSmem* sm, long long
     Key fmax;
     bool have_f = T.nF > 0;
     if (have_f) fmax = sm->F[T.nF - 1];
-    bool toF = valid && (T.nB == 0 || (have_f && klt(key, fmax)));
+    bool toF = valid && ((T.nB == 0 && nRun == 0) || (have_f && klt(key, fmax)));
     bool toB = valid && !toF;
     unsigned bm = __ballot_sync(FULL, toB);
     if (toB) BK(A)[T.off + T.nB + __popc(bm & lt)] = key;
@@ -330,8 +287,10 @@ __device__ __forceinline__ Key bitonic32(Key x, int lane, bool asc) {
     return x;
 }
 
-// Move the 32 smallest BACK keys (or all of them) behind the FRONT.
-__device__ __noinline__ int2 refill(const KArgs* Ap, WarpSmem* sm, long long off, int nF, int nB) {
+// Move the 32 smallest keys of BACK + RUN (or all of them) behind the FRONT.
+// Returns {nF, nB, keys taken from the RUN}.
+__device__ __noinline__ int4 refill(const KArgs* Ap, WarpSmem* sm, long long off, int nF, int nB, const Key* run,
+                                    int nRun) {
     const KArgs& A = *Ap;
     const int lane = threadIdx.x & 31;
     QState T{off, nF, nB};
@@ -350,30 +309,46 @@ __device__ __noinline__ int2 refill(const KArgs* Ap, WarpSmem* sm, long long off
             if (lower ? klt(y, S) : klt(S, y)) S = y;
         }
     }
-    int K = T.nB < 32 ? T.nB : 32;
+    Key r = kinf();  // the RUN's next 32 keys are its 32 smallest (ascending)
+    if (nRun > 0) {
+        if (lane < nRun) r = run[lane];
+        Key rr = kshfl(r, 31 - lane);                  // descending
+        if (klt(rr, S)) S = rr;                        // 32 smallest of both, bitonic
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {
+            Key y = kshfl_xor(S, j);
+            bool lower = (lane & j) == 0;
+            if (lower ? klt(y, S) : klt(S, y)) S = y;
+        }
+    }
+    const int avail = T.nB + nRun;
+    int K = avail < 32 ? avail : 32;
     if (lane < K) sm->F[T.nF + lane] = S;
     Key thr = kshfl(S, K - 1);
     __syncwarp();
     T.nF += K;
-    // compact the BACK, dropping the K selected keys (all <= thr)
-    const unsigned lt = lanemask_lt();
-    int w = 0;
-    for (int base = 0; base < T.nB; base += 32) {
-        int i = base + lane;
-        Key x;
-        bool keep = false;
-        if (i < T.nB) {
-            x = BK(A)[T.off + i];
-            keep = klt(thr, x);
+    const int from_run = nRun > 0 ? __popc(__ballot_sync(FULL, lane < nRun && !klt(thr, r))) : 0;
+    if (K > from_run) {
+        // compact the BACK, dropping the selected keys (all <= thr)
+        const unsigned lt = lanemask_lt();
+        int w = 0;
+        for (int base = 0; base < T.nB; base += 32) {
+            int i = base + lane;
+            Key x;
+            bool keep = false;
+            if (i < T.nB) {
+                x = BK(A)[T.off + i];
+                keep = klt(thr, x);
+            }
+            unsigned km = __ballot_sync(FULL, keep);
+            __syncwarp();
+            if (keep) BK(A)[T.off + w + __popc(km & lt)] = x;
+            w += __popc(km);
+            __syncwarp();
         }
-        unsigned km = __ballot_sync(FULL, keep);
-        __syncwarp();
-        if (keep) BK(A)[T.off + w + __popc(km & lt)] = x;
-        w += __popc(km);
-        __syncwarp();
+        T.nB = w;
     }
-    T.nB = w;
-    return make_int2(T.nF, T.nB);
+    return make_int4(T.nF, T.nB, from_run, 0);
 }
 
 // ---- logging ---------------------------------------------------------------
@@ -624,49 +599,45 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         unsigned long long dig = 0ull;
         long long peak = 0;
 
-        // ---- init (engine.py:183-199): records, f_t, pre-filter, pending list
-        T.npend = 0;
-        int nuns = 0;
-        long long tokens = 0;
-        for (int base = 0; base < n; base += 32) {
-            int i = base + lane;
-            bool v = i < n;
-            bool serv = false;
-            if (v) {
-                long long g = T.off + i;
-                const uint32_t prompt = A.in.prompt_len[g], mid = A.in.pred_len[g];
-                uint4 st;
-                st.x = prompt;
-                st.y = A.in.true_output_len[g];
-                tokens += st.y;
-                st.z = mid;
-                st.w = ((uint32_t)A.in.pred_urgency[g] << 24) | A.in.tie_rank[g];
-                STA(A)[g] = st;
-                serv = (long long)prompt + 1 <= cap;
-                store_dyn(A, g, remaining_time(prompt, mid, 0, 0, 0, P), 0u, serv ? ST_WAIT : ST_UNS);
-                A.out.req.first_scheduled[g] = __longlong_as_double(0x7ff8000000000000ll);
-                A.out.req.finish_time[g] = __longlong_as_double(0x7ff8000000000000ll);
-                A.out.req.evictions[g] = 0u;
+        // ---- init (engine.py:183-199). Records, f_t and output slots were
+        // written grid-wide by the prepass (ss_prepass.cu); here only the
+        // pending list when some request is unservable (pre-filter, :193-199)
+        T.nRun = 0;
+        const int bulkP = A.w.bulkP[t];
+        const bool dense = A.w.nuns[t] == 0u;
+        int nuns = 0, bulk = 0;
+        if (dense) {
+            T.npend = n;  // pending index == slot
+            bulk = bulkP;
+        } else {
+            T.npend = 0;
+            for (int base = 0; base < n; base += 32) {
+                int i = base + lane;
+                bool v = i < n;
+                bool serv = v && (long long)A.in.prompt_len[T.off + i] + 1 <= cap;
+                unsigned sm_ = __ballot_sync(FULL, serv), um = __ballot_sync(FULL, v && !serv);
+                if (serv) A.w.pend[T.off + T.npend + __popc(sm_ & lt)] = (uint32_t)i;
+                if (v && !serv) A.out.unservable_slots[T.off + nuns + __popc(um & lt)] = (uint32_t)i;
+                bulk += __popc(__ballot_sync(FULL, serv && i < bulkP));
+                T.npend += __popc(sm_);
+                nuns += __popc(um);
             }
-            unsigned sm_ = __ballot_sync(FULL, v && serv), um = __ballot_sync(FULL, v && !serv);
-            if (v && serv) A.w.pend[T.off + T.npend + __popc(sm_ & lt)] = (uint32_t)i;
-            if (v && !serv) A.out.unservable_slots[T.off + nuns + __popc(um & lt)] = (uint32_t)i;
-            T.npend += __popc(sm_);
-            nuns += __popc(um);
         }
-        if (lane == 0) c.nuns = nuns;
+        if (lane == 0) {
+            c.nuns = nuns;
+            c.dense = dense ? 1 : 0;
+            c.bulk = bulkP > 0 ? bulk : 0;
+            c.rbase = A.w.eoff[t];
+            c.rpos = 0;
+        }
         // round cap: params.max_rounds, or automatic (the reference has no guard
         // and can cycle forever under some tight-memory schedules)
-        tokens += __shfl_xor_sync(FULL, tokens, 16);
-        tokens += __shfl_xor_sync(FULL, tokens, 8);
-        tokens += __shfl_xor_sync(FULL, tokens, 4);
-        tokens += __shfl_xor_sync(FULL, tokens, 2);
-        tokens += __shfl_xor_sync(FULL, tokens, 1);
+        const long long tokens = (long long)A.w.tok[t];
         long long round_cap = A.P.max_rounds > 0 ? A.P.max_rounds : 64 * (tokens + n) + 100000;
         if (round_cap > 0x7fffffffll) round_cap = 0x7fffffffll;
         T.cursor = 0;
         __syncwarp();
-        T.next_ready = T.npend > 0 ? A.in.ready_time[T.off + A.w.pend[T.off]] : INFINITY;
+        T.next_ready = T.npend > 0 ? A.in.ready_time[T.off + (dense ? 0 : A.w.pend[T.off])] : INFINITY;
 
         Key okey;  // key of the ongoing record in OM[lane] (lane < nO)
 
@@ -675,13 +646,20 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             // admission of prediction-ready requests (engine.py:204-206)
             const double thr = ss::add(T.clock, 1e-12);
             if (T.next_ready <= thr) {
+                if (T.cursor == 0 && c.bulk > 0) {
+                    // bulk admission: the group is already queued (F_Q set by the
+                    // prepass) as this trace's sorted RUN
+                    T.cursor = c.bulk;
+                    T.nRun = c.bulk;
+                }
+                const bool dn = c.dense != 0;
                 while (T.cursor < T.npend) {
                     int i = T.cursor + lane;
                     bool v = i < T.npend;
                     uint32_t s = 0;
                     bool ok = false;
                     if (v) {
-                        s = A.w.pend[T.off + i];
+                        s = dn ? (uint32_t)i : A.w.pend[T.off + i];
                         ok = A.in.ready_time[T.off + s] <= thr;
                     }
                     unsigned am = __ballot_sync(FULL, ok);
@@ -695,24 +673,31 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         const uint32_t w = STA(A)[g].w;
                         k = make_key<POL>(w >> 24, DYN(A)[g].ft, w & SLOT_MASK, s, false);
                     }
-                    const int2 qs = q_insert32(&A, sm, T.off, T.nF, T.nB, k, mine);
+                    const int2 qs = q_insert32(&A, sm, T.off, T.nF, T.nB, T.nRun, k, mine);
                     T.nF = qs.x;
                     T.nB = qs.y;
                     T.cursor += cnt;
                     if (cnt < 32) break;
                 }
-                T.next_ready = T.cursor < T.npend ? A.in.ready_time[T.off + A.w.pend[T.off + T.cursor]] : INFINITY;
+                T.next_ready = T.cursor < T.npend
+                                   ? A.in.ready_time[T.off + (dn ? T.cursor : A.w.pend[T.off + T.cursor])]
+                                   : INFINITY;
             }
-            const int live = T.nF + T.nB + T.nO;
+            const int live = T.nF + T.nB + T.nO + T.nRun;
             if (live == 0) {
                 if (T.cursor >= T.npend) break;
                 T.clock = T.next_ready;
                 continue;
             }
-            if (T.nF < b && T.nB > 0) {
-                const int2 qs = refill(&A, sm, T.off, T.nF, T.nB);
+            if (T.nF < b && (T.nB > 0 || T.nRun > 0)) {
+                const int4 qs = refill(&A, sm, T.off, T.nF, T.nB,
+                                       reinterpret_cast<const Key*>(A.w.S) + c.rbase + c.rpos, T.nRun);
                 T.nF = qs.x;
                 T.nB = qs.y;
+                T.nRun -= qs.z;
+                __syncwarp();
+                if (lane == 0) c.rpos += qs.z;
+                __syncwarp();
             }
             if (lane == 0) c.s_pool += live;
 
@@ -867,7 +852,10 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 T.nins += __popc(pm);
             }
             __syncwarp();
-            if (T.status != SS_TRACE_OK) break;
+            if (T.status != SS_TRACE_OK) {
+                T.rounds += 1;  // the raising round counts (oracle / golden convention)
+                break;
+            }
             MemS mem;
             mem.slot = 0xFFFFFFFFu;
             const bool act = lane < m;
@@ -884,6 +872,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             // a completed request popped from a stale entry: estimate_kv_size raises
             if (anom && __ballot_sync(FULL, act && (mem.flg & F_STAGE) == ST_DONE)) {
                 set_status(T, SS_TRACE_REF_ERROR);
+                T.rounds += 1;
                 break;
             }
 
@@ -1226,7 +1215,10 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         }
                         __syncwarp();
                     }
-                    if (T.status != SS_TRACE_OK) break;
+                    if (T.status != SS_TRACE_OK) {
+                        T.rounds += 1;
+                        break;
+                    }
                     if (g_act) {  // every copy sees the final state
                         const Dyn d = DYN(A)[T.off + mem.slot];
                         mem.dec = d.dec;
@@ -1332,7 +1324,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         *fp = *fp & ~F_INS;
                     }
                 }
-                const int2 qs = q_insert32(&A, sm, T.off, T.nF, T.nB, k, v);
+                const int2 qs = q_insert32(&A, sm, T.off, T.nF, T.nB, T.nRun, k, v);
                 T.nF = qs.x;
                 T.nB = qs.y;
             }
@@ -1414,23 +1406,44 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
 // --------------------------------------------------------------------------
 static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-size_t work_bytes(int64_t n) {
-    size_t nn = (size_t)(n > 0 ? n : 1);
-    // st, dy, B, ins: 16 B; rpos, R, pend: 4 B
-    return 4 * align16(nn * 16) + 3 * align16(nn * 4) + 16;
+static long long tiles_for(int64_t n) { return ((n > 0 ? n : 1) + RS_TILE - 1) / RS_TILE; }
+
+// Layout: zero-initialised block first (one memset per run), then scratch.
+size_t work_bytes(int64_t n, int32_t T) {
+    size_t nn = (size_t)(n > 0 ? n : 1), tt = (size_t)(T > 0 ? T : 1);
+    size_t zero = align16(tt * 8) + align16(tt * 4) + align16((size_t)RS_PASSES * 256 * 4) + 16;
+    // st, dy, B, ins, S: 16 B; rpos, R, pend, tt0, tt1: 4 B
+    return zero + 5 * align16(nn * 16) + 5 * align16(nn * 4) + align16(tt * 4) + align16((tt + 1) * 8) +
+           align16((size_t)(RS_PASSES + 1) * 4) + align16((size_t)256 * tiles_for(n) * 4);
 }
 
-void carve_work(void* base, int64_t n, Work* w) {
-    size_t nn = (size_t)(n > 0 ? n : 1);
+size_t work_zero_bytes(int32_t T) {
+    size_t tt = (size_t)(T > 0 ? T : 1);
+    return align16(tt * 8) + align16(tt * 4) + align16((size_t)RS_PASSES * 256 * 4) + 16;
+}
+
+void carve_work(void* base, int64_t n, int32_t T, Work* w) {
+    size_t nn = (size_t)(n > 0 ? n : 1), tt = (size_t)(T > 0 ? T : 1);
     char* p = (char*)base;
+    w->tok = (unsigned long long*)p; p += align16(tt * 8);
+    w->nuns = (uint32_t*)p;  p += align16(tt * 4);
+    w->hist = (uint32_t*)p;  p += align16((size_t)RS_PASSES * 256 * 4);
+    w->next_trace = (int*)p; p += 16;
     w->st = (void*)p;        p += align16(nn * 16);
     w->dy = (void*)p;        p += align16(nn * 16);
     w->B = (void*)p;         p += align16(nn * 16);
     w->ins = (void*)p;       p += align16(nn * 16);
+    w->S = (void*)p;         p += align16(nn * 16);
     w->rpos = (uint32_t*)p;  p += align16(nn * 4);
     w->R = (uint32_t*)p;     p += align16(nn * 4);
     w->pend = (uint32_t*)p;  p += align16(nn * 4);
-    w->next_trace = (int*)p;
+    w->tt0 = (uint32_t*)p;   p += align16(nn * 4);
+    w->tt1 = (uint32_t*)p;   p += align16(nn * 4);
+    w->bulkP = (int*)p;      p += align16(tt * 4);
+    w->eoff = (long long*)p; p += align16((tt + 1) * 8);
+    w->plan = (int*)p;       p += align16((size_t)(RS_PASSES + 1) * 4);
+    w->tcnt = (uint32_t*)p;
+    w->tiles_max = tiles_for(n);
 }
 
 int sched_smem_bytes() { return (int)(sizeof(WarpSmem) * WPB); }

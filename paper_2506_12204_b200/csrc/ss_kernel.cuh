@@ -17,7 +17,19 @@ struct Work {
     void* B;             // queue BACK: 16-byte packed keys
     uint32_t* R;         // resident list (eviction candidates)
     uint32_t* pend;      // servable requests in pending order
-    void* ins;           // this round's re-queue list: 16-byte keys
+    void* ins;           // this round's re-queue list: 16-byte keys (prepass: sort ping-pong)
+    // ---- prepass (ss_prepass.cu) -------------------------------------------
+    void* S;                  // sorted bulk runs: 16-byte keys, trace t at [eoff[t], eoff[t] + bulkP[t])
+    uint32_t* tt0;            // radix sort payload: trace index of each key (ping-pong pair)
+    uint32_t* tt1;
+    unsigned long long* tok;  // per trace: sum of true output lengths (round cap)
+    uint32_t* nuns;           // per trace: unservable requests (0 -> identity pending list)
+    int* bulkP;               // per trace: bulk prefix length (0: no bulk admission)
+    long long* eoff;          // per trace + 1: exclusive scan of bulkP
+    uint32_t* hist;           // [RS_PASSES][256] global digit histograms
+    int* plan;                // [RS_PASSES] source buffer of each pass (-1: skipped), [RS_PASSES]: final
+    uint32_t* tcnt;           // [256][tiles] per-tile digit counts -> scanned offsets
+    long long tiles_max;      // capacity of tcnt in tiles
     int* next_trace;     // work counter for persistent warps
 };
 
@@ -28,8 +40,16 @@ struct KArgs {
     Work w;
 };
 
-size_t work_bytes(int64_t n_requests);
-void carve_work(void* base, int64_t n_requests, Work* w);
+constexpr int PP_THREADS = 256;               // prepass CTA size
+constexpr int RS_ITEMS = 16;                  // radix sort: keys per thread per tile
+constexpr int RS_TILE = PP_THREADS * RS_ITEMS;
+constexpr int RS_PASSES = 16;                 // 8-bit digits: lo 4, hi 8, trace index 4
+
+size_t work_bytes(int64_t n_requests, int32_t n_traces);
+void carve_work(void* base, int64_t n_requests, int32_t n_traces, Work* w);
+size_t work_zero_bytes(int32_t n_traces);  // leading bytes of the workspace zeroed per run
+// grid-wide prepass: request init, per-trace tallies, bulk-admission sort
+int launch_prepass(const KArgs& a, void* stream);
 int launch_sched(const KArgs& a, int blocks, void* stream);
 int sched_smem_bytes();
 int sched_max_blocks(int policy, int* sm_count);

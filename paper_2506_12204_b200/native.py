@@ -50,15 +50,23 @@ def lib():
                                     C.POINTER(C.c_float)]
         L.ss_run_traces_host.argtypes = [C.POINTER(A.ss_params), C.POINTER(A.ss_trace_batch),
                                          C.POINTER(A.ss_outputs), C.c_void_p, C.POINTER(C.c_float)]
+        L.ss_last_timings.argtypes = [C.POINTER(C.c_float), C.POINTER(C.c_float)]
         for f in ("ss_device_info", "ss_workspace_bytes", "ss_kernel_config", "ss_run_traces",
-                  "ss_run_traces_host"):
+                  "ss_run_traces_host", "ss_last_timings"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
 
 
 EXPORTED = ("ss_last_error", "ss_device_info", "ss_workspace_bytes", "ss_run_traces",
-            "ss_run_traces_host", "ss_kernel_config")
+            "ss_run_traces_host", "ss_kernel_config", "ss_last_timings")
+
+
+def last_timings():
+    """(prepass_ms, kernel_ms) of this thread's last timed ss_run_traces."""
+    pm, km = C.c_float(), C.c_float()
+    lib().ss_last_timings(C.byref(pm), C.byref(km))
+    return pm.value, km.value
 
 
 def last_error() -> str:

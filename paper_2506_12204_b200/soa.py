@@ -63,6 +63,15 @@ class TraceBatch:
         if (self.prompt < 1).any() or (self.true_out < 1).any():
             raise ValueError("lengths must be >= 1")
 
+    def subset(self, traces: Sequence[int]) -> "TraceBatch":
+        """A new batch holding the listed traces, in that order."""
+        parts = []
+        for t in traces:
+            s = self.trace_slice(int(t))
+            kw = {f: getattr(self, f)[s] for f in FIELDS + ("ids", "record_pos")}
+            parts.append(TraceBatch(offsets=np.array([0, s.stop - s.start], np.int64), **kw))
+        return TraceBatch.concat(parts)
+
     @staticmethod
     def concat(batches: Sequence["TraceBatch"]) -> "TraceBatch":
         offs = [np.zeros(1, np.int64)]

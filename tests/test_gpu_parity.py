@@ -46,6 +46,7 @@ def test_gpu_matches_reference_stale_entries(native, case):
     res = native.run_host(case_params(case, A.SS_FLAG_DIGEST), batch, want_log=True)
     if "ref_error" in case["expected"]:
         assert int(res.stats["status"][0]) == A.SS_TRACE_REF_ERROR
+        assert int(res.stats["rounds"][0]) == case["expected"]["rounds_before_error"] + 1
     else:
         check_against_golden(res, case, batch=batch)
 
@@ -67,6 +68,8 @@ def _compare_with_oracle(gpu, cpu, batch):
     """Statuses must agree everywhere; every other field is compared on the
     traces both finished (a reference exception ends a trace mid-round)."""
     assert np.array_equal(gpu.stats["status"], cpu.stats["status"]), "status"
+    # the round that raised counts on both sides (the reference's rounds + 1)
+    assert np.array_equal(gpu.stats["rounds"], cpu.stats["rounds"]), "rounds (incl. failed traces)"
     ok = cpu.stats["status"] == 0
     for k in ("rounds", "evictions", "digest", "completed", "unservable", "mem_used_peak",
               "lost_evictions", "anomalies", "sum_pool", "sum_granted", "sum_victims",
@@ -96,6 +99,26 @@ def test_gpu_many_traces_vs_oracle(native, capacity):
     gpu = native.run_host(p(), batch)
     cpu = run_oracle(p(), batch, threads=8)
     assert _compare_with_oracle(gpu, cpu, batch) >= batch.n_traces // 2
+
+
+def test_gpu_config_d_sample_vs_oracle(native):
+    """Config D at bench shape (1,000 requests, 3 levels, 2,295 slots): heavy
+    eviction, lost decisions, stale heap entries and reference exceptions.
+    Status and rounds must agree on every trace, everything else where the
+    trace finished."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.dist import shard_seeds
+    from paper_2506_12204_b200.results import make_params
+    from paper_2506_12204_b200.tracegen import generate_batch
+    from paper_2506_12204_b200.workload import WorkloadSpec
+
+    batch = generate_batch(WorkloadSpec(total_requests=1000, levels=3), shard_seeds(64, 0), pinned=False)
+    p = lambda: make_params(get_profile("a100_qwen7b"), 16, 2295, levels=3, flags=A.SS_FLAG_DIGEST)
+    gpu = native.run_host(p(), batch)
+    cpu = run_oracle(p(), batch, threads=8)
+    assert (cpu.stats["status"] == A.SS_TRACE_REF_ERROR).any()  # the sample covers an exception
+    _compare_with_oracle(gpu, cpu, batch)
 
 
 @pytest.mark.parametrize("policy", ["fcfs", "sjf", "hpjf"])
@@ -180,3 +203,96 @@ def test_run_dropin_matches_golden(native):
             assert rec.generated_tokens == want[3] and rec.evictions == want[4]
         ends = [e for e in tr.events if e.kind is EventKind.ITERATION_END]
         assert len(ends) == len(exp["log"])
+
+
+# ---- bulk admission: grid-wide radix sort + sorted RUN (ss_prepass.cu) ------
+
+@pytest.mark.parametrize("policy", ["semantic", "fcfs", "sjf", "hpjf"])
+@pytest.mark.parametrize("capacity", [10**9, 1500, 700])
+def test_gpu_bulk_run_forced_vs_oracle(native, policy, capacity):
+    """bulk_min = 1 routes every trace's first admission through the sorted
+    RUN (tiny groups, later arrivals interleaving with the RUN, evictions and
+    stale entries re-queued next to it); results must not change."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.results import make_params
+
+    batch, cfg = _seeded_batch(64, 300, dict(levels=3), seed0=900)
+    p = lambda bm: make_params(cfg.gpu_profile(), 16, capacity, policy=policy, levels=3, flags=A.SS_FLAG_DIGEST,
+                               bulk_min=bm)
+    gpu = native.run_host(p(1), batch)
+    cpu = run_oracle(p(0), batch, threads=8)
+    _compare_with_oracle(gpu, cpu, batch)
+
+
+def _burst_batch(n_traces, n, seed0, levels=5, **kw):
+    """Traces whose requests all arrive at t = 0 (config C's shape, small)."""
+    from paper_2506_12204_b200.tracegen import generate_batch
+    from paper_2506_12204_b200.workload import WorkloadSpec
+
+    spec = WorkloadSpec(total_requests=n, concurrent=n, concurrent_mode="fixed", levels=levels, **kw)
+    return generate_batch(spec, list(range(seed0, seed0 + n_traces)))
+
+
+@pytest.mark.parametrize("capacity", [10**9, 3000, 600])
+def test_gpu_bulk_burst_vs_oracle(native, capacity):
+    """Several traces of 2,000 requests at t = 0 (default bulk threshold):
+    multi-trace segmented sort, the RUN feeding the FRONT for the whole trace."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.results import make_params
+
+    batch = _burst_batch(6, 2000, 40)
+    p = lambda bm: make_params(get_profile("a100_qwen7b"), 16, capacity, levels=5, flags=A.SS_FLAG_DIGEST,
+                               bulk_min=bm)
+    gpu = native.run_host(p(0), batch)
+    cpu = run_oracle(p(0), batch, threads=8)
+    _compare_with_oracle(gpu, cpu, batch)
+    off = native.run_host(p(-1), batch)  # bulk path disabled: same results
+    assert np.array_equal(off.stats["digest"], gpu.stats["digest"])
+
+
+def test_gpu_bulk_with_unservable_vs_oracle(native):
+    """A bulk group containing unservable requests (prompt + 1 > capacity):
+    non-identity pending list, unservable keys sorted behind the RUN."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.results import make_params
+
+    batch = _burst_batch(3, 1500, 7, levels=3)
+    p = make_params(get_profile("a100_qwen7b"), 8, 100, levels=3, flags=A.SS_FLAG_DIGEST, bulk_min=0)
+    gpu = native.run_host(p, batch)
+    cpu = run_oracle(p, batch, threads=8)
+    assert cpu.stats["unservable"].min() > 0
+    _compare_with_oracle(gpu, cpu, batch)
+
+
+def test_gpu_bulk_round_logs_vs_oracle(native):
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.results import make_params
+
+    batch = _burst_batch(2, 1200, 3, levels=3)
+    mk = lambda fl: make_params(get_profile("a5000_qwen7b"), 16, 1800, levels=3,
+                                flags=fl)
+    gpu = native.run_host(mk(A.SS_FLAG_DIGEST), batch, want_log=True)
+    cpu = run_oracle(mk(A.SS_FLAG_DIGEST | A.SS_FLAG_ROUND_LOG), batch)
+    for t in range(batch.n_traces):
+        assert cpu.stats["status"][t] == gpu.stats["status"][t]
+        if cpu.stats["status"][t] == 0:
+            assert np.array_equal(gpu.logs[t], cpu.logs[t]), t
+
+
+def test_gpu_pool_100k_capped_vs_oracle(native):
+    """Config C's shape at 100k requests: the first 3,000 rounds (round cap)
+    agree with the oracle round for round (digest + rounds)."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.results import make_params
+
+    batch = _burst_batch(1, 100_000, 1)
+    p = make_params(get_profile("a100_qwen7b"), 16, 10**9, levels=5, flags=A.SS_FLAG_DIGEST, max_rounds=3000)
+    gpu = native.run_host(p, batch)
+    cpu = run_oracle(p, batch)
+    for k in ("status", "rounds", "digest", "completed"):
+        assert gpu.stats[k][0] == cpu.stats[k][0], k
+    assert int(gpu.stats["status"][0]) == A.SS_TRACE_ROUND_CAP
