@@ -62,6 +62,15 @@ EXPORTED = ("ss_last_error", "ss_device_info", "ss_workspace_bytes", "ss_run_tra
             "ss_run_traces_host", "ss_kernel_config", "ss_last_timings")
 
 
+# kernels one ss_run_traces call launches (ss_prepass.cu + the scheduler):
+# detect, eoff scan, init, bulk keys, histogram, plan, 16 x (count, scan,
+# scatter), final copy, sched_kernel. The bulk stages exit at once when no
+# trace admits a bulk group.
+def launches_per_run(params=None) -> int:
+    bulk = params is None or params.bulk_min >= 0
+    return 3 + (3 + 16 * 3 + 1 if bulk else 0) + 1
+
+
 def last_timings():
     """(prepass_ms, kernel_ms) of this thread's last timed ss_run_traces."""
     pm, km = C.c_float(), C.c_float()
