@@ -699,6 +699,141 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 if (lane == 0) c.rpos += qs.z;
                 __syncwarp();
             }
+            // ---- fast path: a stretch of same-batch decode rounds --------------
+            // 99.5% of config-B rounds (96% under config D's tight memory) keep the
+            // batch equal to the ongoing set: p* is an ongoing (decoding) request,
+            // no queued decoding request is eligible (batching.py:73-88), nobody
+            // needs eviction and nobody completes. Such rounds run here with the
+            // members in registers, record writes deferred to the stretch's end and
+            // the same arithmetic, digest terms and bookkeeping as the general
+            // round below (engine.py:288-380), which handles every other round.
+            if (POL == SS_POLICY_SEMANTIC && !anom && T.nO > 0 && T.nO <= b) {
+                const int nc0 = T.nF < b ? T.nF : b;
+                const bool cdec = lane < nc0 && (sm->F[lane].aux & DEC_BIT);
+                if (!__any_sync(FULL, cdec)) {
+                    const Key F0 = T.nF > 0 ? sm->F[0] : kinf();
+                    const int m = T.nO;
+                    const bool act = lane < m;
+                    MemS mem;
+                    if (act) mem = sm->OM[lane];
+                    // rounds before the first completion (a lane completes when dec + 1 >= tout)
+                    int left = __reduce_min_sync(FULL, act ? (int)(m_tout(mem) - mem.dec) - 1 : 0x7fffffff);
+                    unsigned nmax = __reduce_max_sync(FULL, act ? m_prompt(mem) + mem.dec + 1u : 0u);
+                    // KV admission (engine.py:296-327) of an all-decode batch: immediate 1,
+                    // exclusive scan = lane, demand = max(est, 1) with est non-increasing
+                    // over the stretch; below safe_used no member can need an eviction
+                    long long est0 = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
+                    const int maxdem = (int)__reduce_max_sync(FULL, (unsigned)(est0 > 1 ? est0 : 1));
+                    const long long safe_used = cap - (long long)maxdem - m;
+                    Key ok0 = kshfl(okey, 0);
+                    int k = 0;
+                    for (;;) {
+                        if (left <= 0) break;                                       // completion round
+                        if (T.next_ready <= ss::add(T.clock, 1e-12)) break;         // admission due
+                        if (!klt(ok0, F0)) break;                                   // p* is queued (prefill)
+                        if (T.used > safe_used) {
+                            long long e = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
+                            long long dem = e > 1 ? e : 1;
+                            if (dem + lane > cap) dem = 1;
+                            if (__any_sync(FULL, act && dem + lane + T.used > cap)) break;  // eviction
+                        }
+                        double part;  // batch_duration (engine.py:126-149) of an all-decode batch
+                        if (!A.P.decode_cost_sum) {
+                            part = decode_step_time((long long)nmax, 1, P);
+                        } else {
+                            const double st = act ? decode_step_time((long long)m_prompt(mem) + mem.dec + 1, 1, P) : 0.0;
+                            PySum ps;
+                            ps.init();
+                            for (int q = 0; q < m; q++) ps.push(__shfl_sync(FULL, st, q));
+                            part = ps.value();
+                        }
+                        const double end = ss::add(T.clock, ss::add(0.0, part));
+                        if (act) {
+                            mem.dec += 1u;
+                            mem.ft = remaining_time(m_prompt(mem), m_mid(mem), m_prompt(mem), mem.dec, 0, P);
+                        }
+                        T.used += m;
+                        if (want_digest) {
+                            const unsigned long long r64 = (unsigned long long)T.rounds;
+                            const bool hl = lane >= 29;
+                            const uint32_t htag = lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME);
+                            const unsigned long long hval =
+                                lane == 31 ? ss_hdr_word(SS_KIND_DECODE, m, 0, 0)
+                                           : (lane == 30 ? (unsigned long long)T.used : dbits(end));
+                            const unsigned long long term = act ? ss_term(r64, SS_TAG_GRANT, lane, mem.slot)
+                                                                : ss_term(r64, htag, 0, hval);
+                            dig += (act || hl) ? term : 0ull;
+                            if (m > 29 && hl && act) dig += ss_term(r64, htag, 0, hval);
+                        }
+                        if (logging) {
+                            const long long lp = c.logpos;
+                            if (act) log_put(c, lp + SS_LOG_HEADER_WORDS + lane, mem.slot);
+                            __syncwarp();
+                            if (lane == 0) {
+                                const unsigned long long mu = (unsigned long long)T.used, tb = dbits(end);
+                                log_put(c, lp + 0, (uint32_t)SS_KIND_DECODE);
+                                log_put(c, lp + 1, (uint32_t)m);
+                                log_put(c, lp + 2, 0u);
+                                log_put(c, lp + 3, 0u);
+                                log_put(c, lp + 4, (uint32_t)mu);
+                                log_put(c, lp + 5, (uint32_t)(mu >> 32));
+                                log_put(c, lp + 6, (uint32_t)tb);
+                                log_put(c, lp + 7, (uint32_t)(tb >> 32));
+                                c.logpos = lp + SS_LOG_HEADER_WORDS + m;
+                            }
+                            __syncwarp();
+                        }
+                        if (T.used > peak) peak = T.used;
+                        T.clock = end;
+                        T.rounds += 1;
+                        nmax += 1u;
+                        left -= 1;
+                        k += 1;
+                        // the ongoing set stays sorted by key (usually already is)
+                        if (act) okey = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, true);
+                        const Key nx = kshfl_down(okey, 1);
+                        if (__ballot_sync(FULL, lane + 1 < m && klt(nx, okey))) {
+                            if (act) sm->X[32 + lane] = okey;
+                            __syncwarp();
+                            int r = 0;
+                            for (int q = 0; q < m; q++) r += klt(sm->X[32 + q], okey) ? 1 : 0;
+                            __syncwarp();
+                            if (act) {
+                                sm->OM[r] = mem;
+                                sm->X[32 + r] = okey;
+                            }
+                            __syncwarp();
+                            if (act) {
+                                mem = sm->OM[lane];
+                                okey = sm->X[32 + lane];
+                            }
+                            __syncwarp();
+                        }
+                        ok0 = kshfl(okey, 0);
+                        if (logging && c.logpos > c.logcap) {
+                            set_status(T, SS_TRACE_LOG_OVERFLOW);
+                            break;
+                        }
+                        if (T.rounds >= round_cap) {
+                            set_status(T, SS_TRACE_ROUND_CAP);
+                            break;
+                        }
+                    }
+                    if (k > 0) {
+                        if (act) {
+                            store_dyn(A, T.off + mem.slot, mem.ft, mem.dec, mem.flg);
+                            sm->OM[lane] = mem;
+                            sm->X[32 + lane] = okey;
+                        }
+                        if (lane == 0) {
+                            c.s_pool += (long long)live * k;
+                            c.s_granted += (long long)m * k;
+                        }
+                        __syncwarp();
+                        continue;
+                    }
+                }
+            }
             if (lane == 0) c.s_pool += live;
 
             // ---- stage-aware composition (batching.py:46-88)
