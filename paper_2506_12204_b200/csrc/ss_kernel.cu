@@ -102,6 +102,13 @@ __device__ __forceinline__ Key kshfl_xor(const Key& k, int m) {
     r.aux = __shfl_xor_sync(FULL, k.aux, m);
     return r;
 }
+// A branch on a warp-uniform value that the compiler cannot prove uniform
+// (smem / global loads, call results, loop-carried counters) makes ptxas guard
+// every later shuffle and vote of the loop with a divergence check (BRA.DIV)
+// and an out-of-line collective fallback. Routing such conditions through a
+// vote makes them provably uniform: no guards, a third less code.
+__device__ __forceinline__ bool uni(bool x) { return __all_sync(0xffffffffu, x); }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -253,7 +260,7 @@ __device__ __noinline__ int2 q_insert32(const KArgs* Ap, WarpSmem* sm, long long
 
 // Remove FRONT entries flagged in `rm` (bit i = FRONT[i]).
 __device__ void f_compact(const Env& E, Trace& T, unsigned long long rm) {
-    if (rm == 0ull) return;
+    if (uni(rm == 0ull)) return;
     WarpSmem* sm = E.sm;
     const int lane = E.lane;
     const unsigned lt = lanemask_lt();
@@ -295,7 +302,7 @@ __device__ __noinline__ int4 refill(const KArgs* Ap, WarpSmem* sm, long long off
     const int lane = threadIdx.x & 31;
     QState T{off, nF, nB};
     Key S = kinf();  // running top-32, ascending across lanes
-    for (int base = 0; base < T.nB; base += 32) {
+    for (int base = 0; uni(base < T.nB); base += 32) {
         int i = base + lane;
         Key x = i < T.nB ? BK(A)[T.off + i] : kinf();
         Key smax = kshfl(S, 31);
@@ -310,7 +317,7 @@ __device__ __noinline__ int4 refill(const KArgs* Ap, WarpSmem* sm, long long off
         }
     }
     Key r = kinf();  // the RUN's next 32 keys are its 32 smallest (ascending)
-    if (nRun > 0) {
+    if (uni(nRun > 0)) {
         if (lane < nRun) r = run[lane];
         Key rr = kshfl(r, 31 - lane);                  // descending
         if (klt(rr, S)) S = rr;                        // 32 smallest of both, bitonic
@@ -327,12 +334,12 @@ __device__ __noinline__ int4 refill(const KArgs* Ap, WarpSmem* sm, long long off
     Key thr = kshfl(S, K - 1);
     __syncwarp();
     T.nF += K;
-    const int from_run = nRun > 0 ? __popc(__ballot_sync(FULL, lane < nRun && !klt(thr, r))) : 0;
-    if (K > from_run) {
+    const int from_run = __popc(__ballot_sync(FULL, lane < nRun && !klt(thr, r)));
+    if (uni(K > from_run)) {
         // compact the BACK, dropping the selected keys (all <= thr)
         const unsigned lt = lanemask_lt();
         int w = 0;
-        for (int base = 0; base < T.nB; base += 32) {
+        for (int base = 0; uni(base < T.nB); base += 32) {
             int i = base + lane;
             Key x;
             bool keep = false;
@@ -369,7 +376,7 @@ __device__ __forceinline__ void set_status(Trace& T, int st) {
 
 // Index of slot v's live entry in this round's re-queue list, or -1.
 __device__ int ins_find(const KArgs& A, const Trace& T, uint32_t v, int lane) {
-    for (int base = 0; base < T.nins; base += 32) {
+    for (int base = 0; uni(base < T.nins); base += 32) {
         int i = base + lane;
         bool hit = i < T.nins && (INS(A)[T.off + i].aux & SLOT_MASK) == v;
         unsigned hm = __ballot_sync(FULL, hit);
@@ -384,8 +391,8 @@ __device__ void q_delete(const Env& E, Trace& T, Round& R, uint32_t v, uint32_t 
     const KArgs& A = *E.A;
     WarpSmem* sm = E.sm;
     const int lane = E.lane;
-    if (!(flg & F_Q)) return;
-    if (flg & F_INS) {
+    if (uni(!(flg & F_Q))) return;
+    if (uni(flg & F_INS)) {
         int idx = ins_find(A, T, v, lane);
         if (idx >= 0 && lane == 0) INS(A)[T.off + idx].aux = SLOT_MASK;  // dead entry
         __syncwarp();
@@ -400,13 +407,13 @@ __device__ void q_delete(const Env& E, Trace& T, Round& R, uint32_t v, uint32_t 
         return;
     }
     int found = -1;
-    for (int base = 0; base < T.nB && found < 0; base += 32) {
+    for (int base = 0; uni(base < T.nB && found < 0); base += 32) {
         int i = base + lane;
         bool hit = i < T.nB && (BK(A)[T.off + i].aux & SLOT_MASK) == v;
         unsigned hm = __ballot_sync(FULL, hit);
         if (hm) found = base + __ffs(hm) - 1;
     }
-    if (found >= 0) {
+    if (uni(found >= 0)) {
         if (lane == 0) BK(A)[T.off + found] = BK(A)[T.off + T.nB - 1];
         T.nB -= 1;
     }
@@ -426,7 +433,7 @@ SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot,
     Key best;
     bool have = false;
     int best_ri = -1;
-    for (int base = 0; base < T.nR; base += 32) {
+    for (int base = 0; uni(base < T.nR); base += 32) {
         int i = base + lane;
         if (i < T.nR) {
             uint32_t s = A.w.R[T.off + i];
@@ -455,7 +462,7 @@ SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot,
             best_ri = ori;
         }
     }
-    if (!have) return false;
+    if (uni(!have)) return false;
     const uint32_t v = best.aux & SLOT_MASK;
     const long long gv = T.off + v;
     // ---- should_recompute (kvcache.py:81-134), evaluated redundantly per lane
@@ -483,7 +490,7 @@ SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot,
     const Key nkey = make_key<POL>(m_rank(vm), fta, m_tie(vm), v, false);
     // heap: delete_by_id if queued, then insert with the new key
     int ins_idx = -1;
-    if ((flg & F_Q) && (flg & F_INS)) ins_idx = ins_find(A, T, v, lane);
+    if (uni((flg & F_Q) && (flg & F_INS))) ins_idx = ins_find(A, T, v, lane);
     else q_delete(E, T, R, v, flg);
     const uint32_t nflg = (flg & ~(F_STAGE | F_PF)) | ST_WAIT | (pf ? F_PF : 0u) | F_Q | F_INS;
     if (lane == 0) {
@@ -519,7 +526,7 @@ SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot,
         }
         c.s_victims += 1;
     }
-    if (ins_idx < 0) T.nins += 1;
+    if (uni(ins_idx < 0)) T.nins += 1;
     T.nR -= 1;
     R.ndec += 1;
     __syncwarp();
@@ -573,7 +580,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         int t = 0;
         if (lane == 0) t = atomicAdd(A.w.next_trace, 1);
         t = __shfl_sync(FULL, t, 0);
-        if (t >= A.in.n_traces) break;
+        if (uni(t >= A.in.n_traces)) break;
 
         Trace T;
         T.off = A.in.trace_offsets[t];
@@ -606,12 +613,12 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         const int bulkP = A.w.bulkP[t];
         const bool dense = A.w.nuns[t] == 0u;
         int nuns = 0, bulk = 0;
-        if (dense) {
+        if (uni(dense)) {
             T.npend = n;  // pending index == slot
             bulk = bulkP;
         } else {
             T.npend = 0;
-            for (int base = 0; base < n; base += 32) {
+            for (int base = 0; uni(base < n); base += 32) {
                 int i = base + lane;
                 bool v = i < n;
                 bool serv = v && (long long)A.in.prompt_len[T.off + i] + 1 <= cap;
@@ -642,18 +649,18 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         Key okey;  // key of the ongoing record in OM[lane] (lane < nO)
 
         // ---- the round loop (engine.py:202-224)
-        while (T.status == SS_TRACE_OK) {
+        while (uni(T.status == SS_TRACE_OK)) {
             // admission of prediction-ready requests (engine.py:204-206)
             const double thr = ss::add(T.clock, 1e-12);
-            if (T.next_ready <= thr) {
-                if (T.cursor == 0 && c.bulk > 0) {
+            if (uni(T.next_ready <= thr)) {
+                if (uni(T.cursor == 0 && c.bulk > 0)) {
                     // bulk admission: the group is already queued (F_Q set by the
                     // prepass) as this trace's sorted RUN
                     T.cursor = c.bulk;
                     T.nRun = c.bulk;
                 }
                 const bool dn = c.dense != 0;
-                while (T.cursor < T.npend) {
+                while (uni(T.cursor < T.npend)) {
                     int i = T.cursor + lane;
                     bool v = i < T.npend;
                     uint32_t s = 0;
@@ -684,12 +691,12 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                    : INFINITY;
             }
             const int live = T.nF + T.nB + T.nO + T.nRun;
-            if (live == 0) {
-                if (T.cursor >= T.npend) break;
+            if (uni(live == 0)) {
+                if (uni(T.cursor >= T.npend)) break;
                 T.clock = T.next_ready;
                 continue;
             }
-            if (T.nF < b && (T.nB > 0 || T.nRun > 0)) {
+            if (uni(T.nF < b && (T.nB > 0 || T.nRun > 0))) {
                 const int4 qs = refill(&A, sm, T.off, T.nF, T.nB,
                                        reinterpret_cast<const Key*>(A.w.S) + c.rbase + c.rpos, T.nRun);
                 T.nF = qs.x;
@@ -707,7 +714,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             // members in registers, record writes deferred to the stretch's end and
             // the same arithmetic, digest terms and bookkeeping as the general
             // round below (engine.py:288-380), which handles every other round.
-            if (POL == SS_POLICY_SEMANTIC && !anom && T.nO > 0 && T.nO <= b) {
+            if (POL == SS_POLICY_SEMANTIC && uni(!anom && T.nO > 0 && T.nO <= b)) {
                 const int nc0 = T.nF < b ? T.nF : b;
                 const bool cdec = lane < nc0 && (sm->F[lane].aux & DEC_BIT);
                 if (!__any_sync(FULL, cdec)) {
@@ -728,23 +735,23 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     Key ok0 = kshfl(okey, 0);
                     int k = 0;
                     for (;;) {
-                        if (left <= 0) break;                                       // completion round
-                        if (T.next_ready <= ss::add(T.clock, 1e-12)) break;         // admission due
-                        if (!klt(ok0, F0)) break;                                   // p* is queued (prefill)
-                        if (T.used > safe_used) {
+                        if (uni(left <= 0)) break;                                  // completion round
+                        if (uni(T.next_ready <= ss::add(T.clock, 1e-12))) break;    // admission due
+                        if (uni(!klt(ok0, F0))) break;                              // p* is queued (prefill)
+                        if (uni(T.used > safe_used)) {
                             long long e = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
                             long long dem = e > 1 ? e : 1;
                             if (dem + lane > cap) dem = 1;
                             if (__any_sync(FULL, act && dem + lane + T.used > cap)) break;  // eviction
                         }
                         double part;  // batch_duration (engine.py:126-149) of an all-decode batch
-                        if (!A.P.decode_cost_sum) {
+                        if (uni(!A.P.decode_cost_sum)) {
                             part = decode_step_time((long long)nmax, 1, P);
                         } else {
                             const double st = act ? decode_step_time((long long)m_prompt(mem) + mem.dec + 1, 1, P) : 0.0;
                             PySum ps;
                             ps.init();
-                            for (int q = 0; q < m; q++) ps.push(__shfl_sync(FULL, st, q));
+                            for (int q = 0; uni(q < m); q++) ps.push(__shfl_sync(FULL, st, q));
                             part = ps.value();
                         }
                         const double end = ss::add(T.clock, ss::add(0.0, part));
@@ -796,7 +803,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             if (act) sm->X[32 + lane] = okey;
                             __syncwarp();
                             int r = 0;
-                            for (int q = 0; q < m; q++) r += klt(sm->X[32 + q], okey) ? 1 : 0;
+                            for (int q = 0; uni(q < m); q++) r += klt(sm->X[32 + q], okey) ? 1 : 0;
                             __syncwarp();
                             if (act) {
                                 sm->OM[r] = mem;
@@ -810,16 +817,16 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             __syncwarp();
                         }
                         ok0 = kshfl(okey, 0);
-                        if (logging && c.logpos > c.logcap) {
+                        if (logging && uni(c.logpos > c.logcap)) {
                             set_status(T, SS_TRACE_LOG_OVERFLOW);
                             break;
                         }
-                        if (T.rounds >= round_cap) {
+                        if (uni(T.rounds >= round_cap)) {
                             set_status(T, SS_TRACE_ROUND_CAP);
                             break;
                         }
                     }
-                    if (k > 0) {
+                    if (uni(k > 0)) {
                         if (act) {
                             store_dyn(A, T.off + mem.slot, mem.ft, mem.dec, mem.flg);
                             sm->OM[lane] = mem;
@@ -858,7 +865,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             // in the reference: equal keys are copies of the same request)
             Key pmin = kinf();
             if (POL != SS_POLICY_SEMANTIC) {
-            } else if (!anom) {
+            } else if (uni(!anom)) {
                 if (T.nO > 0) pmin = sm->X[32];
                 if (nc > 0 && klt(sm->F[0], pmin)) pmin = sm->F[0];
             } else {
@@ -882,7 +889,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 // ongoing first in their order, then the popped candidates
                 cnt_o = lane;
                 cnt_c = T.nO + lane;
-            } else if (!anom) {
+            } else if (uni(!anom)) {
                 // both lists sorted: rank = own index + lower_bound in the other
                 cnt_o = lane;
                 if (cmask) {
@@ -912,13 +919,13 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 if (c_elig) sm->X[lane] = ck;
                 if (has_o) sm->X[32 + lane] = okey;
                 __syncwarp();
-                for (int k = 0; k < nc; k++) {
+                for (int k = 0; uni(k < nc); k++) {
                     if (!((cmask >> k) & 1u)) continue;
                     Key x = sm->X[k];
                     if (c_elig && (klt(x, ck) || (keq(x, ck) && k < lane))) cnt_c++;
                     if (has_o && (klt(x, okey) || keq(x, okey))) cnt_o++;
                 }
-                for (int k = 0; k < T.nO; k++) {
+                for (int k = 0; uni(k < T.nO); k++) {
                     Key x = sm->X[32 + k];
                     if (c_elig && klt(x, ck)) cnt_c++;
                     if (has_o && (klt(x, okey) || (keq(x, okey) && k < lane))) cnt_o++;
@@ -943,7 +950,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 sm->M[cnt_c] = cm;
             }
             if (!direct && has_o && cnt_o < m) sm->M[cnt_o] = sm->OM[lane];
-            if (anom) {
+            if (uni(anom)) {
                 // candidates not selected are pushed back with their current key;
                 // a stale stored key is replaced (heaps.py insert after pop)
                 const bool refresh = has_c && !c_sel && !keq(ck, sm->F[lane]);
@@ -964,7 +971,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     pm &= pm - 1;
                     const uint32_t s = sm->OM[k].slot;
                     const uint32_t f = *FLG(A, T.off + s);
-                    if (f & F_Q) {
+                    if (uni(f & F_Q)) {
                         set_status(T, SS_TRACE_REF_ERROR);
                         break;
                     }
@@ -987,7 +994,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 T.nins += __popc(pm);
             }
             __syncwarp();
-            if (T.status != SS_TRACE_OK) {
+            if (uni(T.status != SS_TRACE_OK)) {
                 T.rounds += 1;  // the raising round counts (oracle / golden convention)
                 break;
             }
@@ -1005,7 +1012,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             const int nO_start = T.nO;
             const int nuns_start = c.nuns;
             // a completed request popped from a stale entry: estimate_kv_size raises
-            if (anom && __ballot_sync(FULL, act && (mem.flg & F_STAGE) == ST_DONE)) {
+            if (uni(anom) && __ballot_sync(FULL, act && (mem.flg & F_STAGE) == ST_DONE)) {
                 set_status(T, SS_TRACE_REF_ERROR);
                 T.rounds += 1;
                 break;
@@ -1034,7 +1041,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 const unsigned mmask = m >= 32 ? FULL : ((1u << m) - 1u);
                 const int f = nm ? __ffs(nm) - 1 : m;
                 R.G = (f >= 32 ? FULL : ((1u << f) - 1u)) & mmask;
-                if (anom) {
+                if (uni(anom)) {
                     // grants of still-queued requests (stale heap entry) before f
                     const unsigned qa = __ballot_sync(FULL, ((R.G >> lane) & 1u) && (mem.flg & F_Q));
                     if (qa && lane == 0) c.anomalies += __popc(qa);
@@ -1046,7 +1053,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     if ((R.G >> lane) & 1u) flg_update(A, T.off + mem.slot, 0u, F_GRANT);
                     __syncwarp();
                     if (act) mem.flg = *FLG(A, T.off + mem.slot);
-                    for (int k = f; k < m && T.status == SS_TRACE_OK; k++) {
+                    for (int k = f; uni(k < m && T.status == SS_TRACE_OK); k++) {
                         if ((R.evmask >> k) & 1u) continue;
                         q = mem_q(mem);
                         const long long imm_k = __shfl_sync(FULL, q.imm, k);
@@ -1061,18 +1068,18 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         if (lane == 0) c.dpend = 0ull;
                         __syncwarp();
                         bool ok = true;
-                        while (demand + T.used > cap) {
-                            if (!evict_one<POL>(E, T, R, slot_k, m, mem, vcall)) {
+                        while (uni(demand + T.used > cap)) {
+                            if (uni(!evict_one<POL>(E, T, R, slot_k, m, mem, vcall))) {
                                 ok = false;
                                 break;
                             }
                         }
                         const uint32_t flg_k = __shfl_sync(FULL, mem.flg, k);
-                        if (!ok) {
+                        if (uni(!ok)) {
                             // AdmissionFailure: evictions stand, their records are lost
                             if (lane == 0) c.lost += R.ndec - d0;
                             R.ndec = d0;
-                            if (kvd_k + imm_k > cap) {
+                            if (uni(kvd_k + imm_k > cap)) {
                                 // _mark_unservable (engine.py:402-412)
                                 q_delete(E, T, R, slot_k, flg_k);
                                 const bool isdec_k = (flg_k & F_STAGE) == ST_DEC;
@@ -1095,7 +1102,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                 __syncwarp();
                                 // every batch copy of it sees the new state
                                 if (act && mem.slot == slot_k) mem.flg = *FLG(A, T.off + slot_k);
-                            } else if (!(flg_k & F_Q)) {
+                            } else if (uni(!(flg_k & F_Q))) {
                                 if (lane == k) {
                                     const Key kk = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, q.isdec);
                                     flg_update(A, T.off + mem.slot, 0u, F_Q | F_INS);
@@ -1111,7 +1118,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         // success: commit this call's decisions
                         R.evmask |= vcall;
                         if (lane == 0) dig += c.dpend;
-                        if (flg_k & F_Q) {
+                        if (uni(flg_k & F_Q)) {
                             // granted while it still has a heap entry (a victim whose
                             // decision was lost): the reference keeps that stale entry
                             if (lane == 0) c.anomalies += 1;
@@ -1125,8 +1132,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     }
                 }
             }
-            if (T.status != SS_TRACE_OK) break;
-            if (anom) {
+            if (uni(T.status != SS_TRACE_OK)) break;
+            if (uni(anom)) {
                 // copies of one request must agree before duration and execution
                 __syncwarp();
                 if (act) {
@@ -1144,7 +1151,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 c.s_granted += ng;
             }
 
-            if (ng == 0) {
+            if (uni(ng == 0)) {
                 // nothing granted (engine.py:329-344): clock does not advance
                 T.nO = 0;
                 if (want_digest && lane == 0) {
@@ -1178,7 +1185,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 if (pre) {
                     const double rl = reload_time(q.kvh, P);
                     const double pft = prefill_time((long long)m_prompt(mem) - q.pfn, P);
-                    for (int k = 0; k < m; k++) {
+                    for (int k = 0; uni(k < m); k++) {
                         const double a = __shfl_sync(FULL, rl, k), c2 = __shfl_sync(FULL, pft, k);
                         if ((pre >> k) & 1u) {
                             total = ss::add(total, a);
@@ -1189,7 +1196,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 const unsigned dm = __ballot_sync(FULL, g_act && q.isdec);
                 if (dm) {
                     double part;
-                    if (!A.P.decode_cost_sum) {
+                    if (uni(!A.P.decode_cost_sum)) {
                         // gamma1 >= 0: the step time is monotone in the context length,
                         // so the max step is the step of the longest context
                         const unsigned nmax =
@@ -1201,7 +1208,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                               : 0.0;
                         PySum ps;
                         ps.init();
-                        for (int k = 0; k < m; k++) {
+                        for (int k = 0; uni(k < m); k++) {
                             const double x = __shfl_sync(FULL, st, k);
                             if ((dm >> k) & 1u) ps.push(x);
                         }
@@ -1214,7 +1221,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 // ---- per-member progress (engine.py:351-363, 382-421)
                 bool done = false;
                 bool dups = false;
-                if (anom) {
+                if (uni(anom)) {
                     const unsigned dupm = __match_any_sync(FULL, g_act ? mem.slot : (0x80000000u | lane));
                     dups = __ballot_sync(FULL, g_act && __popc(dupm) > 1) != 0;
                 }
@@ -1281,7 +1288,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     // duplicate copies of a request: execute copies one by one,
                     // each seeing the previous copy's effect
                     unsigned gm = R.G;
-                    while (gm && T.status == SS_TRACE_OK) {
+                    while (uni(gm && T.status == SS_TRACE_OK)) {
                         const int k = __ffs(gm) - 1;
                         gm &= gm - 1;
                         int err = 0, dn = 0, nres = 0;
@@ -1326,7 +1333,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         alloc = __shfl_sync(FULL, alloc, k);
                         rel = __shfl_sync(FULL, rel, k);
                         const uint32_t s = __shfl_sync(FULL, mem.slot, k);
-                        if (err || alloc > cap - T.used) {
+                        if (uni(err || alloc > cap - T.used)) {
                             set_status(T, SS_TRACE_REF_ERROR);
                             break;
                         }
@@ -1350,7 +1357,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         }
                         __syncwarp();
                     }
-                    if (T.status != SS_TRACE_OK) {
+                    if (uni(T.status != SS_TRACE_OK)) {
                         T.rounds += 1;
                         break;
                     }
@@ -1421,7 +1428,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 if (POL != SS_POLICY_FCFS &&
                     __ballot_sync(FULL, lane + 1 < T.nO && klt(sm->X[32 + ((lane + 1) & 31)], okey))) {
                     int r = 0;
-                    for (int k = 0; k < T.nO; k++) {
+                    for (int k = 0; uni(k < T.nO); k++) {
                         const Key x = sm->X[32 + k];
                         if (klt(x, okey) || (keq(x, okey) && k < lane)) r++;
                     }
@@ -1446,7 +1453,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             //      round's pushed-back / failed / evicted requests with the key
             //      they were queued with (the heap stores keys at insert time)
             f_compact(E, T, R.rmF);
-            for (int base = 0; base < T.nins; base += 32) {
+            for (int base = 0; uni(base < T.nins); base += 32) {
                 const int i = base + lane;
                 bool v = false;
                 Key k;
@@ -1470,7 +1477,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         {
             PySum acc;
             acc.init();
-            for (int base = 0; base < n; base += 32) {
+            for (int base = 0; uni(base < n); base += 32) {
                 const int i = base + lane;
                 double w = 0.0, nw = 0.0;
                 bool fin = false;
