@@ -732,20 +732,25 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     long long est0 = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
                     const int maxdem = (int)__reduce_max_sync(FULL, (unsigned)(est0 > 1 ? est0 : 1));
                     const long long safe_used = cap - (long long)maxdem - m;
-                    Key ok0 = kshfl(okey, 0);
+                    // remaining_time of a decoding member (costs.py:174-191): reload(0)
+                    // and prefill(0) are the same constants every round
+                    const double z0 = ss::add(reload_time(0, P), prefill_time(0, P));
+                    const bool sum_mode = A.P.decode_cost_sum != 0;
                     int k = 0;
                     for (;;) {
-                        if (uni(left <= 0)) break;                                  // completion round
-                        if (uni(T.next_ready <= ss::add(T.clock, 1e-12))) break;    // admission due
-                        if (uni(!klt(ok0, F0))) break;                              // p* is queued (prefill)
+                        // one vote for every exit: a completion, an admission due, p*
+                        // queued (no ongoing key below the queue front), round cap / log
+                        const bool other = left <= 0 || T.next_ready <= ss::add(T.clock, 1e-12) ||
+                                           T.rounds >= round_cap || (logging && c.logpos > c.logcap);
+                        if (__all_sync(FULL, other || !(act && klt(okey, F0)))) break;
                         if (uni(T.used > safe_used)) {
-                            long long e = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
+                            long long e = (long long)m_mid(mem) - (long long)mem.dec;
                             long long dem = e > 1 ? e : 1;
                             if (dem + lane > cap) dem = 1;
                             if (__any_sync(FULL, act && dem + lane + T.used > cap)) break;  // eviction
                         }
                         double part;  // batch_duration (engine.py:126-149) of an all-decode batch
-                        if (uni(!A.P.decode_cost_sum)) {
+                        if (uni(!sum_mode)) {
                             part = decode_step_time((long long)nmax, 1, P);
                         } else {
                             const double st = act ? decode_step_time((long long)m_prompt(mem) + mem.dec + 1, 1, P) : 0.0;
@@ -755,22 +760,32 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             part = ps.value();
                         }
                         const double end = ss::add(T.clock, ss::add(0.0, part));
-                        if (act) {
-                            mem.dec += 1u;
-                            mem.ft = remaining_time(m_prompt(mem), m_mid(mem), m_prompt(mem), mem.dec, 0, P);
+                        // every lane computes; only lanes < m are members
+                        mem.dec += 1u;
+                        {
+                            long long lft = (long long)m_mid(mem) - (long long)mem.dec;
+                            if (lft < 1) lft = 1;
+                            mem.ft = ss::add(z0, decode_total_time((long long)m_prompt(mem) + mem.dec, lft, P));
                         }
                         T.used += m;
                         if (want_digest) {
                             const unsigned long long r64 = (unsigned long long)T.rounds;
                             const bool hl = lane >= 29;
-                            const uint32_t htag = lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME);
-                            const unsigned long long hval =
-                                lane == 31 ? ss_hdr_word(SS_KIND_DECODE, m, 0, 0)
-                                           : (lane == 30 ? (unsigned long long)T.used : dbits(end));
-                            const unsigned long long term = act ? ss_term(r64, SS_TAG_GRANT, lane, mem.slot)
-                                                                : ss_term(r64, htag, 0, hval);
+                            const uint32_t tag = act ? SS_TAG_GRANT
+                                                     : (lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME));
+                            const unsigned long long val =
+                                act ? (unsigned long long)mem.slot
+                                    : (lane == 31 ? ss_hdr_word(SS_KIND_DECODE, m, 0, 0)
+                                                  : (lane == 30 ? (unsigned long long)T.used : dbits(end)));
+                            const unsigned long long term = ss_term(r64, tag, act ? lane : 0, val);
                             dig += (act || hl) ? term : 0ull;
-                            if (m > 29 && hl && act) dig += ss_term(r64, htag, 0, hval);
+                            if (m > 29 && hl && act) {
+                                const uint32_t htag = lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME);
+                                const unsigned long long hval =
+                                    lane == 31 ? ss_hdr_word(SS_KIND_DECODE, m, 0, 0)
+                                               : (lane == 30 ? (unsigned long long)T.used : dbits(end));
+                                dig += ss_term(r64, htag, 0, hval);
+                            }
                         }
                         if (logging) {
                             const long long lp = c.logpos;
@@ -790,14 +805,14 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             }
                             __syncwarp();
                         }
-                        if (T.used > peak) peak = T.used;
+                        peak = T.used > peak ? T.used : peak;
                         T.clock = end;
                         T.rounds += 1;
                         nmax += 1u;
                         left -= 1;
                         k += 1;
                         // the ongoing set stays sorted by key (usually already is)
-                        if (act) okey = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, true);
+                        okey = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, true);
                         const Key nx = kshfl_down(okey, 1);
                         if (__ballot_sync(FULL, lane + 1 < m && klt(nx, okey))) {
                             if (act) sm->X[32 + lane] = okey;
@@ -816,16 +831,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             }
                             __syncwarp();
                         }
-                        ok0 = kshfl(okey, 0);
-                        if (logging && uni(c.logpos > c.logcap)) {
-                            set_status(T, SS_TRACE_LOG_OVERFLOW);
-                            break;
-                        }
-                        if (uni(T.rounds >= round_cap)) {
-                            set_status(T, SS_TRACE_ROUND_CAP);
-                            break;
-                        }
                     }
+                    if (uni(T.rounds >= round_cap)) set_status(T, SS_TRACE_ROUND_CAP);
+                    if (logging && uni(c.logpos > c.logcap)) set_status(T, SS_TRACE_LOG_OVERFLOW);
                     if (uni(k > 0)) {
                         if (act) {
                             store_dyn(A, T.off + mem.slot, mem.ft, mem.dec, mem.flg);
