@@ -265,6 +265,74 @@ int ss_last_timings(float* prepass_ms, float* kernel_ms);
 int ss_kernel_config(const ss_params* params, int32_t n_traces, int* blocks,
                      int* warps_per_block, int* smem_bytes_per_block);
 
+/* ---- per-step entry points (ss_step.cu) -----------------------------------
+ * The reference's public per-step functions, for callers that drive their own
+ * loop over heaps of Request objects (the Python shim's batching / kvcache
+ * modules). HOST buffers in and out; the call stages them through a device
+ * workspace, runs, and synchronises. */
+
+/* A key tuple of the reference (requests.py:81-97): (urgency rank, remaining
+ * seconds, arrival, id), a baseline policy's shorter tuple (engine.py:114-123)
+ * padded with -inf, or an eviction key (every component negated). Compared
+ * lexicographically with IEEE `<`; equal tuples keep pool order. */
+typedef struct ss_key4 { double k[4]; } ss_key4;
+
+#define SS_SELECT_TOP_B        0  /* extract_top_b only            batching.py:46-54  */
+#define SS_SELECT_STAGE_AWARE  1  /* stage_aware_schedule          batching.py:57-88  */
+#define SS_SELECT_PREEMPTIVE   2  /* SJF / HPJF top-b of the merge engine.py:270-285  */
+#define SS_SELECT_FCFS         3  /* ongoing + b - |ongoing| pops  engine.py:256-267  */
+
+/* Replaces extract_top_b / stage_aware_schedule (batching.py:46-88) and the
+ * baselines' selection (engine.py:256-285).
+ *   stored[n_pool]   the dispatch heap's keys as stored at insertion: pop order
+ *   current[n_pool]  key_fn(r) now (p* and merge order); NULL = same as stored
+ *   pool_decoding    1 where r.stage is DECODING (batching.py:39-43)
+ *   ongoing[n_ongoing], ongoing_decoding: the ongoing requests, current keys
+ * Out: cand[<= b]  pool indices of the popped candidates, in pop order;
+ *      merged[<= b + n_ongoing] the merge in batch order, entries j < n_cand
+ *        name candidate j, entries >= n_cand name ongoing (j - n_cand);
+ *      n_selected = members taken (min(b, n_merged)); kind SS_KIND_PREFILL /
+ *        SS_KIND_DECODE. Candidates absent from merged were pushed back as
+ *        prefill work; merged[n_selected:] are pushed back (batching.py:80-87).
+ * b and n_ongoing <= SS_MAX_BATCH. */
+int ss_select_batch(const ss_key4* stored, const ss_key4* current, const uint8_t* pool_decoding,
+                    int64_t n_pool, const ss_key4* ongoing, const uint8_t* ongoing_decoding,
+                    int32_t n_ongoing, int32_t b, int32_t mode, int32_t* cand, int32_t* n_cand,
+                    int32_t* merged, int32_t* n_merged, int32_t* n_selected, int32_t* kind,
+                    void* stream);
+
+/* One eviction decision (kvcache.py:59-67) plus the victim's new counters. */
+typedef struct ss_victim {
+    int32_t index;            /* resident index in the call's arrays            */
+    int32_t action;           /* 0 offload, 1 discard (prefill_action)          */
+    int64_t decode_saved, decode_discarded, freed_slots;
+    int64_t prefilled;        /* prefilled_tokens after the decision             */
+    int64_t kv_host;          /* kv_host_tokens after the decision               */
+    double  f_t_before, f_t_after;
+    int64_t _pad;
+} ss_victim;
+
+/* Replaces priority_based_eviction (kvcache.py:137-179) with should_recompute
+ * (kvcache.py:81-134) applied to every victim.
+ *   ev_keys[n]: the eviction heap's stored keys (smallest pops first);
+ *   per resident: prompt_len, prefilled_tokens, decoded_tokens,
+ *   kv_device_tokens, predicted representative length, f_t; protected[n].
+ *   select = 1: the eviction loop — pop in key order, skip protected, evict
+ *     until demand + used <= capacity; *failed = 1 when every unprotected
+ *     resident went and it still does not fit (AdmissionFailure; the victims
+ *     stand). skipped[] = protected entries popped (re-inserted by the caller).
+ *   select = 0: should_recompute on every entry, in the given order.
+ * victims[] are in eviction order. */
+int ss_evict(const ss_key4* ev_keys, const uint32_t* prompt, const uint32_t* prefilled,
+             const uint32_t* decoded, const uint32_t* kv_device, const uint32_t* pred_len,
+             const double* f_t, const uint8_t* protected_, int64_t n, int64_t demand, int64_t used,
+             int64_t capacity, const ss_profile* profile, int32_t dependency_rule, int32_t select,
+             ss_victim* victims, int64_t* n_victims, int32_t* skipped, int64_t* n_skipped,
+             int32_t* failed, void* stream);
+
+/* Message of the calling thread's last failed per-step call. */
+const char* ss_step_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif
