@@ -330,6 +330,20 @@ int ss_evict(const ss_key4* ev_keys, const uint32_t* prompt, const uint32_t* pre
              ss_victim* victims, int64_t* n_victims, int32_t* skipped, int64_t* n_skipped,
              int32_t* failed, void* stream);
 
+/* Completion-order constraint audit, Eq. 2 (metrics.constraint_audit,
+ * metrics.py:59-91), for many traces at once. Trace t owns records
+ * [offsets[t], offsets[t+1]) in any order; finish = NaN marks a request that
+ * did not complete (excluded, as in the reference). rank = true or predicted
+ * urgency rank. Out: violations[t], comparable[t] (violation_rate =
+ * violations / comparable, 0 if none comparable). pairs (nullable): when
+ * given, receives 2 x sum(violations) int64 (id_a, id_b) in the reference's
+ * order (traces in order; within a trace by the stable finish-time order of
+ * a, then of b); pairs_cap is its length in int64s. HOST pointers. */
+int ss_audit_host(int32_t n_traces, const int64_t* offsets, const double* finish, const double* arrival,
+                  const int32_t* rank, const int64_t* ids, int64_t* violations, int64_t* comparable,
+                  int64_t* pairs, int64_t pairs_cap, void* stream);
+const char* ss_audit_last_error(void);
+
 /* Message of the calling thread's last failed per-step call. */
 const char* ss_step_last_error(void);
 
