@@ -259,18 +259,110 @@ def pool_bench(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def audit_bench(args, wl):
+    """Eq. 2 constraint audit (metrics.py:59-91) of every trace of config B's
+    schedule: pairs examined per second (the reference's n(n-1)/2 per trace)."""
+    from paper_2506_12204_b200 import _abi as A
+    from paper_2506_12204_b200 import native
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.metrics import _audit_call
+    from paper_2506_12204_b200.results import make_params
+
+    base = WORKLOADS["B"]
+    batch, T = build_batch(base, 0, args.traces, pinned=False)
+    sizes = np.diff(batch.offsets)
+    if args.impl == "reference":
+        from oracle_binding import audit_oracle
+
+        res = None
+    else:
+        res = native.run_host(make_params(get_profile(base["profile"]), 16, base["capacity"], levels=base["levels"],
+                                          flags=A.SS_FLAG_DIGEST), batch)
+    # the schedule's finish times (NaN = not completed); the reference arm
+    # needs them too, so it takes them from one device run when available
+    fin = res.finish_time if res is not None else None
+    if fin is None:
+        from oracle_binding import run_oracle
+
+        sub = batch.subset(range(min(T, 16)))
+        r = run_oracle(make_params(get_profile(base["profile"]), 16, base["capacity"], levels=base["levels"]), sub,
+                       threads=os.cpu_count() or 1)
+        fin, batch, T = r.finish_time, sub, sub.n_traces
+        sizes = np.diff(batch.offsets)
+    done = np.add.reduceat(~np.isnan(fin), batch.offsets[:-1]) if T else np.zeros(0)
+    pairs = float((done.astype(np.float64) * (done - 1) / 2).sum())
+    rank = batch.true_urg
+    if args.impl == "reference":
+        from oracle_binding import audit_oracle
+
+        ts = []
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            audit_oracle(batch.offsets, fin, batch.arrival, rank)
+            ts.append(time.perf_counter() - t0)
+        v = pairs / float(np.mean(ts))
+        line = {"metric": "constraint-audit pairs/sec", "value": v, "unit": "pairs/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": {"workload": f"Eq. 2 audit of {T} config-B traces", "pairs_per_step": pairs},
+                "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": 1, "kind": "port",
+                                 "sample": f"{T} traces, oracle so_audit (C restatement), 1 thread"},
+                "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    for _ in range(args.warmup):
+        _audit_call(batch.offsets, fin, batch.arrival, rank, batch.ids, False)
+    kms, ems = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        viol, comp, _ = _audit_call(batch.offsets, fin, batch.arrival, rank, batch.ids, False)
+        ems.append(time.perf_counter() - t0)
+        kms.append(_audit_call.kernel_ms)
+    k_ms = float(np.mean(kms))
+    cpu = None
+    parity = None
+    if not args.no_cpu:
+        from oracle_binding import audit_oracle
+
+        S = min(T, 64)
+        sub_off = batch.offsets[: S + 1]
+        n_s = int(sub_off[-1])
+        t0 = time.perf_counter()
+        cv, cc = audit_oracle(sub_off, fin[:n_s], batch.arrival[:n_s], rank[:n_s])
+        dt = time.perf_counter() - t0
+        sp = float((done[:S].astype(np.float64) * (done[:S] - 1) / 2).sum())
+        cpu = {"value": sp / dt, "unit": "pairs/s", "cores": 1, "kind": "port",
+               "sample": f"first {S} of {T} traces, oracle so_audit (C restatement of metrics.py:59-91), 1 thread"}
+        parity = {"traces_checked": S, "violations_and_comparable_match": bool(np.array_equal(cv, viol[:S]) and
+                                                                              np.array_equal(cc, comp[:S]))}
+    h2d = int(batch.offsets.nbytes + fin.nbytes + batch.arrival.nbytes + 4 * len(fin))
+    line = {"metric": "constraint-audit pairs/sec", "value": pairs / (k_ms / 1e3), "unit": "pairs/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": k_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"Eq. 2 audit (true ranks) of the config-B schedule: {T} traces x "
+                                   f"{base['requests']} requests", "pairs_per_step": pairs,
+                       "violations": int(viol.sum()), "comparable": int(comp.sum())},
+            "cpu_baseline": cpu, "parity": parity,
+            "e2e": {"value": pairs / float(np.mean(ems)), "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 16 * T, "ms_per_step": 1e3 * float(np.mean(ems))},
+            "gpu_launches": args.steps}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="B", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="B", choices=sorted(WORKLOADS) + ["audit"])
     ap.add_argument("--traces", type=int, default=None, help="override traces per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--pool-steps", type=int, default=20000, help="config C: steady-state steps per sample")
     args = ap.parse_args()
+    if args.workload == "audit":
+        return audit_bench(args, None)
     wl = WORKLOADS[args.workload]
     if args.workload == "C":
         return pool_bench(args, wl)

@@ -343,6 +343,8 @@ int ss_audit_host(int32_t n_traces, const int64_t* offsets, const double* finish
                   const int32_t* rank, const int64_t* ids, int64_t* violations, int64_t* comparable,
                   int64_t* pairs, int64_t pairs_cap, void* stream);
 const char* ss_audit_last_error(void);
+/* Device time (ms) of the calling thread's last ss_audit_host pair sweep. */
+double ss_audit_last_kernel_ms(void);
 
 /* Message of the calling thread's last failed per-step call. */
 const char* ss_step_last_error(void);

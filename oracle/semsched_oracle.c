@@ -834,3 +834,28 @@ double so_pysum(const double* x, int64_t n) {
     for (int64_t i = 0; i < n; i++) pysum_add(&a, x[i]);
     return pysum_value(&a);
 }
+
+/* metrics.constraint_audit (metrics.py:59-91), counts only: completed
+ * records (finish not NaN) sorted by finish time, every pair a < b with
+ * f_a < f_b is comparable, a violation when f_a >= arrival_b and
+ * rank_a > rank_b. Ties in f are skipped, so the sort order does not change
+ * the counts; this restatement walks all ordered pairs directly. */
+void so_audit(int32_t n_traces, const int64_t* off, const double* fin, const double* arr, const int32_t* rank,
+              int64_t* violations, int64_t* comparable) {
+    for (int32_t t = 0; t < n_traces; t++) {
+        int64_t v = 0, c = 0;
+        for (int64_t i = off[t]; i < off[t + 1]; i++) {
+            const double fi = fin[i];
+            if (isnan(fi)) continue;
+            for (int64_t j = off[t]; j < off[t + 1]; j++) {
+                if (!(fi < fin[j])) continue;
+                c++;
+                if (fi < arr[j]) continue;
+                if (rank[i] <= rank[j]) continue;
+                v++;
+            }
+        }
+        violations[t] = v;
+        comparable[t] = c;
+    }
+}

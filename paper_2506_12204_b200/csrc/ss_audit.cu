@@ -185,6 +185,7 @@ size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 std::mutex g_mu;
 void* g_buf = nullptr;
 size_t g_cap = 0;
+thread_local double g_rows_ms = 0.0;
 
 }  // namespace
 }  // namespace ss
@@ -192,6 +193,8 @@ size_t g_cap = 0;
 extern "C" {
 
 const char* ss_audit_last_error(void) { return ss::g_err; }
+
+double ss_audit_last_kernel_ms(void) { return ss::g_rows_ms; }
 
 int ss_audit_host(int32_t n_traces, const int64_t* offsets, const double* finish, const double* arrival,
                   const int32_t* rank, const int64_t* ids, int64_t* violations, int64_t* comparable,
@@ -259,10 +262,20 @@ int ss_audit_host(int32_t n_traces, const int64_t* offsets, const double* finish
     in.rank = d_r;
     in.n_traces = n_traces;
     const unsigned yb = (unsigned)((maxn + AT - 1) / AT);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
     if (yb > 0) audit_rows<<<dim3((unsigned)T, yb), AT, 0, st>>>(in, d_v, d_c, d_rv, d_rk, want ? 1 : 0);
+    cudaEventRecord(e1, st);
     cudaMemcpyAsync(violations, d_v, T * 8, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(comparable, d_c, T * 8, cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    g_rows_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     if (e != cudaSuccess) return fail(SS_ERR_CUDA, cudaGetErrorString(e));
     if (!want) return SS_OK;
     int64_t total = 0;

@@ -60,7 +60,8 @@ def lib():
 
 EXPORTED = ("ss_last_error", "ss_device_info", "ss_workspace_bytes", "ss_run_traces",
             "ss_run_traces_host", "ss_kernel_config", "ss_last_timings", "ss_select_batch", "ss_evict",
-            "ss_step_last_error", "ss_audit_host", "ss_audit_last_error")
+            "ss_step_last_error", "ss_audit_host", "ss_audit_last_error",
+            "ss_audit_last_kernel_ms")
 
 
 # kernels one ss_run_traces call launches (ss_prepass.cu + the scheduler):

@@ -47,6 +47,8 @@ def lib():
             f = getattr(_lib, name)
             f.restype = res
             f.argtypes = args + [C.POINTER(A.ss_profile)]
+        _lib.so_audit.restype = None
+        _lib.so_audit.argtypes = [C.c_int32] + [C.c_void_p] * 6
         _lib.so_pysum.restype = C.c_double
         _lib.so_pysum.argtypes = [C.c_void_p, C.c_int64]
     return _lib
@@ -94,3 +96,14 @@ def run_oracle(params: A.ss_params, batch, threads: int = 1, use_ids: bool = Tru
     res = collect(batch, outs, log, log_off)
     res.extra["rc"] = rc
     return res
+
+
+def audit_oracle(offsets, finish, arrival, rank):
+    """Eq. 2 counts per trace from the C restatement (test infrastructure)."""
+    T = len(offsets) - 1
+    arr = lambda x, dt: np.ascontiguousarray(np.asarray(x, dt))
+    off, fin, av, rk = arr(offsets, np.int64), arr(finish, np.float64), arr(arrival, np.float64), arr(rank, np.int32)
+    v = np.zeros(max(T, 1), np.int64)
+    c = np.zeros(max(T, 1), np.int64)
+    lib().so_audit(T, _ptr(off), _ptr(fin), _ptr(av), _ptr(rk), v.ctypes.data, c.ctypes.data)
+    return v[:T], c[:T]

@@ -70,3 +70,15 @@ def test_audit_rejects_bad_ranking():
     with pytest.raises(ValueError):
         constraint_audit(Trace(), "bogus")
     assert constraint_audit(Trace(), "true") == ([], 0.0)
+
+
+@pytest.mark.parametrize("case", AUDIT, ids=[c["name"] for c in AUDIT])
+def test_oracle_audit_counts_match_reference(case):
+    """The C restatement (bench CPU baseline) gives the reference's counts."""
+    from oracle_binding import audit_oracle
+
+    recs = [d for d in case["records"] if d[4] is not None]
+    for rk, col in (("true", 7), ("predicted", 8)):
+        v, c = audit_oracle([0, len(recs)], [d[4] for d in recs], [d[1] for d in recs], [d[col] for d in recs])
+        assert int(v[0]) == len(case[f"audit_{rk}"]["pairs"])
+        assert (int(v[0]) / int(c[0]) if c[0] else 0.0) == case[f"audit_{rk}"]["rate"]
