@@ -387,7 +387,24 @@ def main():
 
     t0 = time.perf_counter()
     batch, T = build_batch(wl, rank, args.traces)
-    log(f"[rank {rank}] traces {T} x {wl['requests']} prepared in {time.perf_counter() - t0:.2f} s")
+    host_gen_s = time.perf_counter() - t0
+    log(f"[rank {rank}] traces {T} x {wl['requests']} prepared in {host_gen_s:.2f} s")
+    # the same inputs generated on the device (one thread per trace, straight into HBM)
+    from paper_2506_12204_b200.dist import shard_seeds
+    from paper_2506_12204_b200.tracegen import generate_batch_device
+    from paper_2506_12204_b200.workload import WorkloadSpec
+
+    gspec = WorkloadSpec(total_requests=wl["requests"], levels=wl["levels"])
+    gseeds = shard_seeds(T, rank)
+    generate_batch_device(gspec, gseeds[:64], device=torch.device("cuda", local))  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    gdb = generate_batch_device(gspec, gseeds, device=torch.device("cuda", local))
+    dev_gen_s = time.perf_counter() - t0
+    gen_match = bool(torch.equal(gdb.t["ready"][: batch.n_requests].cpu(), torch.from_numpy(batch.ready)) and
+                     torch.equal(gdb.t["prompt"][: batch.n_requests].cpu(),
+                                 torch.from_numpy(batch.prompt.view(np.int32))))
+    del gdb
     prof = get_profile(wl["profile"])
     pf = lambda: make_params(prof, 16, wl["capacity"], levels=wl["levels"], flags=A.SS_FLAG_DIGEST)
     dbatch = native.DeviceBatch(batch, dev)
@@ -517,6 +534,9 @@ def main():
                        "kernel": {"blocks": cfgk["blocks"], "warps_per_block": cfgk["warps_per_block"],
                                   "smem_per_block": cfgk["smem_per_block"]}},
             "traces_per_s": traces_s,
+            "tracegen": {"host_ms": 1e3 * host_gen_s, "host_threads": os.cpu_count(), "device_ms": 1e3 * dev_gen_s,
+                         "device_matches_host": gen_match,
+                         "note": "input preparation (generate + predictor_pipeline), outside the timed step"},
             "decisions_per_step": int(dec_t.item()) // args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_src, "kernel_ms": k_ms,

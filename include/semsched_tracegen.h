@@ -55,6 +55,15 @@ typedef struct ss_gen_out {         /* [n_traces * total_requests], pending orde
 int ss_generate_traces(const ss_gen_spec* spec, int64_t n_traces, const int64_t* seeds,
                        const int64_t* pred_seeds, const ss_gen_out* out, int n_threads);
 
+/* The same generator on the device: one thread per trace, `out` holds DEVICE
+ * pointers (the scheduler's inputs stay in HBM). seeds / pred_seeds and the
+ * spec's arrays are host memory. Synchronises `stream` (a cudaStream_t, NULL
+ * = default). Returns 0 on success, 1 on an invalid spec, 2 on a CUDA error,
+ * 3 if a trace's ready times are not non-decreasing in generation order (the
+ * generator relies on the FIFO prediction server for the pending order). */
+int ss_generate_traces_device(const ss_gen_spec* spec, int64_t n_traces, const int64_t* seeds,
+                              const int64_t* pred_seeds, const ss_gen_out* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

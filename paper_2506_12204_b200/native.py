@@ -61,7 +61,7 @@ def lib():
 EXPORTED = ("ss_last_error", "ss_device_info", "ss_workspace_bytes", "ss_run_traces",
             "ss_run_traces_host", "ss_kernel_config", "ss_last_timings", "ss_select_batch", "ss_evict",
             "ss_step_last_error", "ss_audit_host", "ss_audit_last_error",
-            "ss_audit_last_kernel_ms")
+            "ss_audit_last_kernel_ms", "ss_generate_traces", "ss_generate_traces_device")
 
 
 # kernels one ss_run_traces call launches (ss_prepass.cu + the scheduler):
@@ -173,6 +173,26 @@ class DeviceBatch:
         self.t = {"offsets": torch.from_numpy(np.ascontiguousarray(batch.offsets)).to(device)}
         for f, _ in self.FIELDS:
             self.t[f] = torch.from_numpy(np.ascontiguousarray(getattr(batch, f))).to(device)
+
+    @classmethod
+    def allocate(cls, n_traces: int, per_trace: int, device="cuda", with_ids: bool = False):
+        """Uninitialised inputs for ``n_traces`` equal-length traces (filled
+        on the device, e.g. by ``tracegen.generate_batch_device``)."""
+        import torch
+
+        self = cls.__new__(cls)
+        self.batch = None
+        self.n_traces = n_traces
+        n = n_traces * per_trace
+        self.n_requests = n
+        dts = {"ready": torch.float64, "arrival": torch.float64, "prompt": torch.int32, "true_out": torch.int32,
+               "pred_len": torch.int32, "pred_urg": torch.uint8, "true_urg": torch.uint8, "tie": torch.int32}
+        self.t = {"offsets": torch.arange(n_traces + 1, dtype=torch.int64, device=device) * per_trace}
+        for f, dt in dts.items():
+            self.t[f] = torch.empty(max(n, 1), dtype=dt, device=device)
+        for f in ("ids", "record_pos"):
+            self.t[f] = torch.empty(max(n, 1) if with_ids else 0, dtype=torch.int64, device=device)
+        return self
 
     def struct(self) -> A.ss_trace_batch:
         db = A.ss_trace_batch()

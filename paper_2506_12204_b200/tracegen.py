@@ -45,14 +45,8 @@ def _lib():
     return L
 
 
-def generate_batch(spec: WorkloadSpec, seeds: Sequence[int], predictor: PredictorConfig = PredictorConfig(),
-                   pred_seeds: Sequence[int] = None, threads: int = 0, pinned: bool = False) -> TraceBatch:
-    """Traces for ``seeds`` (workload seeds); ``pred_seeds`` default to the same
-    values (``run_scenario`` uses ``cfg.seed`` for both)."""
-    seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64))
-    pseeds = seeds if pred_seeds is None else np.ascontiguousarray(np.asarray(pred_seeds, dtype=np.int64))
-    T, N = len(seeds), int(spec.total_requests)
-    n = T * N
+def _gen_spec(spec: WorkloadSpec, predictor: PredictorConfig):
+    """ss_gen_spec for ``spec`` + ``predictor``; returns (spec, keep-alive arrays)."""
     # representative length of every bucket index (workload.py:48-60)
     width = spec.max_output_len / spec.buckets
     reps = np.array([int(round((i + 0.5) * width)) for i in range(spec.buckets)], np.uint32)
@@ -60,7 +54,7 @@ def generate_batch(spec: WorkloadSpec, seeds: Sequence[int], predictor: Predicto
     if spec.urgency_weights:
         weights = np.ascontiguousarray(np.asarray(spec.urgency_weights, np.float64))
     s = ss_gen_spec()
-    s.total_requests = N
+    s.total_requests = int(spec.total_requests)
     s.gap_s = spec.gap_s
     s.concurrent = spec.concurrent
     s.concurrent_fixed = 1 if spec.concurrent_mode == "fixed" else 0
@@ -78,6 +72,53 @@ def generate_batch(spec: WorkloadSpec, seeds: Sequence[int], predictor: Predicto
     s.length_error = predictor.length_error
     s.urgency_disp = ErrorModel(predictor.urgency_error, spec.levels).displacement
     s.length_disp = ErrorModel(predictor.length_error, spec.max_output_len).displacement
+    return s, (reps, weights)
+
+
+def generate_batch_device(spec: WorkloadSpec, seeds: Sequence[int], predictor: PredictorConfig = PredictorConfig(),
+                          pred_seeds: Sequence[int] = None, device="cuda"):
+    """``generate_batch`` on the GPU (``ss_generate_traces_device``, one thread
+    per trace): returns a ``native.DeviceBatch`` whose inputs never leave
+    HBM, identical to ``DeviceBatch(generate_batch(...))``."""
+    import torch
+
+    from .native import DeviceBatch, NativeUnavailable
+
+    seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64))
+    pseeds = seeds if pred_seeds is None else np.ascontiguousarray(np.asarray(pred_seeds, dtype=np.int64))
+    T, N = len(seeds), int(spec.total_requests)
+    s, keep = _gen_spec(spec, predictor)
+    db = DeviceBatch.allocate(T, N, device, with_ids=True)
+    t = db.t
+    o = ss_gen_out(*[t[k].data_ptr() if t[k].numel() else None for k in
+                     ("ready", "arrival", "prompt", "true_out", "pred_len", "pred_urg", "true_urg", "tie",
+                      "ids", "record_pos")])
+    L = _lib()
+    if not getattr(L, "_gen_dev_typed", False):
+        L.ss_generate_traces_device.restype = C.c_int
+        L.ss_generate_traces_device.argtypes = [C.POINTER(ss_gen_spec), C.c_int64, C.c_void_p, C.c_void_p,
+                                                C.POINTER(ss_gen_out), C.c_void_p]
+        L._gen_dev_typed = True
+    rc = L.ss_generate_traces_device(C.byref(s), T, seeds.ctypes.data, pseeds.ctypes.data, C.byref(o),
+                                     C.c_void_p(torch.cuda.current_stream(device).cuda_stream))
+    if rc == 1:
+        raise ValueError("invalid workload spec for the native generator")
+    if rc == 2:
+        raise NativeUnavailable("CUDA error in ss_generate_traces_device")
+    if rc == 3:
+        raise RuntimeError("prediction-ready order differs from generation order")
+    return db
+
+
+def generate_batch(spec: WorkloadSpec, seeds: Sequence[int], predictor: PredictorConfig = PredictorConfig(),
+                   pred_seeds: Sequence[int] = None, threads: int = 0, pinned: bool = False) -> TraceBatch:
+    """Traces for ``seeds`` (workload seeds); ``pred_seeds`` default to the same
+    values (``run_scenario`` uses ``cfg.seed`` for both)."""
+    seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int64))
+    pseeds = seeds if pred_seeds is None else np.ascontiguousarray(np.asarray(pred_seeds, dtype=np.int64))
+    T, N = len(seeds), int(spec.total_requests)
+    n = T * N
+    s, keep = _gen_spec(spec, predictor)
 
     def buf(dt):
         if pinned:
