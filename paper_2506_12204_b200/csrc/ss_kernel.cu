@@ -65,6 +65,7 @@ struct Cold {
     int rpos, bulk;   // RUN cursor; requests admitted in bulk (first round)
     int dense;        // no unservable request: pending index == slot
     int nuns, lost, anomalies, n;
+    int dbg;  // SS_DEBUG_ANOM builds: general-path rounds run with anom set
 };
 
 struct WarpSmem {
@@ -600,7 +601,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 c.log = A.out.round_log + A.out.log_offsets[t];
                 c.logcap = A.out.log_offsets[t + 1] - A.out.log_offsets[t];
             }
-            c.nuns = c.lost = c.anomalies = 0;
+            c.nuns = c.lost = c.anomalies = c.dbg = 0;
             c.n = n;
         }
         unsigned long long dig = 0ull;
@@ -736,6 +737,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     // and prefill(0) are the same constants every round
                     const double z0 = ss::add(reload_time(0, P), prefill_time(0, P));
                     const bool sum_mode = A.P.decode_cost_sum != 0;
+                    // digest: this lane's term tag and position, pre-multiplied (see ss_term)
+                    constexpr unsigned long long DG = 0x9E3779B97F4A7C15ull, DG24 = DG << 24;
+                    const uint32_t dtag = act ? SS_TAG_GRANT : (lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME));
+                    const unsigned long long dgc = ((((unsigned long long)dtag) << 20) ^ (unsigned long long)(act ? lane : 0)) * DG;
+                    unsigned long long dgr = (unsigned long long)T.rounds * DG24;
                     int k = 0;
                     for (;;) {
                         // one vote for every exit: a completion, an admission due, p*
@@ -771,13 +777,14 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         if (want_digest) {
                             const unsigned long long r64 = (unsigned long long)T.rounds;
                             const bool hl = lane >= 29;
-                            const uint32_t tag = act ? SS_TAG_GRANT
-                                                     : (lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME));
                             const unsigned long long val =
                                 act ? (unsigned long long)mem.slot
                                     : (lane == 31 ? ss_hdr_word(SS_KIND_DECODE, m, 0, 0)
                                                   : (lane == 30 ? (unsigned long long)T.used : dbits(end)));
-                            const unsigned long long term = ss_term(r64, tag, act ? lane : 0, val);
+                            // ss_term(r, tag, idx, val) with ((r << 24) ^ c) * G = r * (G << 24) + c * G
+                            // (c < 2^24): the round part advances by one add per round
+                            const unsigned long long term = ss_mix64(val ^ (dgr + dgc));
+                            dgr += DG24;
                             dig += (act || hl) ? term : 0ull;
                             if (m > 29 && hl && act) {
                                 const uint32_t htag = lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME);
@@ -813,7 +820,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         k += 1;
                         // the ongoing set stays sorted by key (usually already is)
                         okey = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, true);
-                        const Key nx = kshfl_down(okey, 1);
+                        Key nx;  // order check needs the next lane's (hi, lo) only
+                        nx.hi = __shfl_down_sync(FULL, okey.hi, 1);
+                        nx.lo = __shfl_down_sync(FULL, okey.lo, 1);
                         if (__ballot_sync(FULL, lane + 1 < m && klt(nx, okey))) {
                             if (act) sm->X[32 + lane] = okey;
                             __syncwarp();
@@ -850,6 +859,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 }
             }
             if (lane == 0) c.s_pool += live;
+#ifdef SS_DEBUG_ANOM
+            if (lane == 0) c.dbg += anom ? 1 : 0;
+#endif
 
             // ---- stage-aware composition (batching.py:46-88)
             // candidates popped from the queue: top-b (semantic / SJF / HPJF,
@@ -1539,7 +1551,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 st->status = T.status;
                 st->lost_evictions = c.lost;
                 st->anomalies = c.anomalies;
+#ifdef SS_DEBUG_ANOM
+                st->_pad = c.dbg;
+#else
                 st->_pad = 0;
+#endif
                 st->sum_pool = c.s_pool;
                 st->sum_granted = c.s_granted;
                 st->sum_victims = c.s_victims;
