@@ -539,6 +539,39 @@ SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot,
     return true;
 }
 
+// Does a stale dispatch-queue entry remain? An entry is stale
+// when its stored key no longer equals the key of the request's current state,
+// the request completed, or it is also an ongoing member; duplicate ongoing
+// copies of one request count too. The sorted RUN holds only untouched bulk
+// arrivals and is never stale.
+template <int POL>
+__device__ __noinline__ bool queue_has_stale(const KArgs* Ap, const WarpSmem* sm, long long off, int nF, int nB,
+                                             int nO) {
+    const KArgs& A = *Ap;
+    const int lane = threadIdx.x & 31;
+    bool st = false;
+    auto check = [&](const Key& k) {
+        const uint32_t s = k.aux & SLOT_MASK;
+        const long long g = off + s;
+        const Dyn d = DYN(A)[g];
+        const uint32_t w = STA(A)[g].w;
+        const Key cur = make_key<POL>(w >> 24, d.ft, w & SLOT_MASK, s, (d.flg & F_STAGE) == ST_DEC);
+        return !keq(cur, k) || cur.aux != k.aux || (d.flg & F_STAGE) == ST_DONE || !(d.flg & F_Q);
+    };
+    if (lane < nF) st |= check(sm->F[lane]);
+    if (lane + 32 < nF) st |= check(sm->F[lane + 32]);
+    for (int base = 0; uni(base < nB); base += 32) {
+        const int i = base + lane;
+        if (i < nB) st |= check(BK(A)[off + i]);
+    }
+    // duplicate ongoing copies of one request (each executes separately)
+    const uint32_t os = lane < nO ? sm->OM[lane].slot : (0x80000000u | (uint32_t)lane);
+    const unsigned same = __match_any_sync(FULL, os);
+    if (lane < nO) st |= __popc(same) > 1;
+    if (lane < nO) st |= (DYN(A)[off + sm->OM[lane].slot].flg & F_Q) != 0;
+    return __any_sync(FULL, st);
+}
+
 // ---- per-lane member quantities (32-bit: token counts of one request) -------
 struct MemQ {
     bool isdec;
@@ -707,6 +740,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 if (lane == 0) c.rpos += qs.z;
                 __syncwarp();
             }
+            // stale entries are transient: once none is left the trace returns to
+            // the exact fast paths (checked every 32 rounds while flagged)
+            if (uni(anom && (T.rounds & 31) == 0) &&
+                !queue_has_stale<POL>(&A, sm, T.off, T.nF, T.nB, T.nO))
+                anom = false;
             // ---- fast path: a stretch of same-batch decode rounds --------------
             // 99.5% of config-B rounds (96% under config D's tight memory) keep the
             // batch equal to the ongoing set: p* is an ongoing (decoding) request,

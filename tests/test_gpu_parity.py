@@ -296,3 +296,23 @@ def test_gpu_pool_100k_capped_vs_oracle(native):
     for k in ("status", "rounds", "digest", "completed"):
         assert gpu.stats[k][0] == cpu.stats[k][0], k
     assert int(gpu.stats["status"][0]) == A.SS_TRACE_ROUND_CAP
+
+
+@pytest.mark.parametrize("cap,levels,n", [(1200, 5, 800), (700, 4, 500)])
+def test_gpu_tight_memory_sweep_vs_oracle(native, cap, levels, n):
+    """256 traces per tight budget: thousands of lost decisions and stale heap
+    entries; the kernel leaves the stale-entry path when none is left
+    (queue_has_stale) and must stay exact."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.dist import shard_seeds
+    from paper_2506_12204_b200.results import make_params
+    from paper_2506_12204_b200.tracegen import generate_batch
+    from paper_2506_12204_b200.workload import WorkloadSpec
+
+    batch = generate_batch(WorkloadSpec(total_requests=n, levels=levels), shard_seeds(256, 0, seed0=17))
+    p = lambda: make_params(get_profile("a100_qwen7b"), 16, cap, levels=levels, flags=A.SS_FLAG_DIGEST)
+    gpu = native.run_host(p(), batch)
+    cpu = run_oracle(p(), batch, threads=8)
+    assert cpu.stats["anomalies"].sum() > 100
+    _compare_with_oracle(gpu, cpu, batch)
