@@ -14,7 +14,9 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 f = None
 hdr = None
 agg = defaultdict(int)
+ins = defaultdict(int)
 tot = 0
+toti = 0
 for row in csv.reader(io.StringIO(out)):
     if not row:
         continue
@@ -29,9 +31,11 @@ for row in csv.reader(io.StringIO(out)):
     d = dict(zip(hdr[2:], row[2:]))
     try:
         s = int(d.get("Warp Stall Sampling (All Samples)", "0") or 0)
+        n_i = int(d.get("Instructions Executed", "0") or 0)
     except ValueError:
         continue
     tot += s
+    toti += n_i
     ln = int(row[0])
     if f == "ss_kernel.cu":
         name = None
@@ -39,7 +43,9 @@ for row in csv.reader(io.StringIO(out)):
             if a <= ln:
                 name = (a, n)
         agg[name] += s
+        ins[name] += n_i
     else:
         agg[(0, f)] += s
+        ins[(0, f)] += n_i
 for k, v in sorted(agg.items(), key=lambda x: -x[1])[:30]:
-    print(f"{100 * v / tot:5.1f}%  {k}")
+    print(f"{100 * v / tot:5.1f}% samples {100 * ins[k] / max(toti, 1):5.1f}% instr  {k}")
