@@ -540,6 +540,10 @@ def main():
             "decisions_per_step": int(dec_t.item()) // args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_src, "kernel_ms": k_ms,
+                         "measured_dram_gbs": (traffic / (k_ms / 1e3) / 1e9) if traffic else None,
+                         "note": "achieved = the survey's HBM pool-scan byte model; the kernel keeps queue fronts and "
+                                 "ongoing sets on chip, so measured DRAM traffic (ncu) is ~1/600 of it and the kernel "
+                                 "is issue/latency-bound (DESIGN.md §6)",
                          "algorithmic_bytes_per_launch": alg,
                          "model": "SURVEY.md §8(d) B_decision summed over this launch's rounds"},
             "cpu_baseline": cpu,
