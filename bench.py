@@ -555,6 +555,7 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()  # rank 0 finishes its CPU baseline and report first
         dist.destroy_process_group()
 
 
