@@ -517,8 +517,9 @@ def main():
         # status and rounds on every sampled trace; the digest where the trace
         # finished (a reference exception ends a trace mid-round)
         ok = res.stats["status"] == 0
+        obs = ok | (res.stats["status"] == A.SS_TRACE_REF_ERROR)
         match = bool(np.array_equal(res.stats["status"], stats["status"][:sample]) and
-                     np.array_equal(res.stats["rounds"], stats["rounds"][:sample]) and
+                     np.array_equal(res.stats["rounds"][obs], stats["rounds"][:sample][obs]) and
                      np.array_equal(res.stats["digest"][ok], stats["digest"][:sample][ok]))
         parity = {"traces_checked": sample, "digest_and_rounds_match": match,
                   "reference_error_traces": int((~ok).sum())}
@@ -550,7 +551,7 @@ def main():
             "parity": parity,
             "e2e": e2e,
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * native.launches_per_run(pf()),
+            "gpu_launches": args.steps * native.launches_per_run(pf(), dbatch.max_trace_len),
             "failed_traces": bad,
         }
         print(json.dumps(line), flush=True)

@@ -194,6 +194,17 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
                    a16((size_t)T * sizeof(ss_trace_stats)) + a16(nn * 4);
     size_t log_b = logr ? a16((size_t)log_words * 4) + a16((T + 1) * 8) : 0;
     size_t ws_b = ss::work_bytes(n, T);
+    // no trace long enough for a bulk first round: skip the bulk-sort stage
+    ss_params pp = *params;
+    if (pp.bulk_min == 0) {
+        int64_t maxlen = 0;
+        for (int32_t t = 0; t < T; t++) {
+            const int64_t k = hb->trace_offsets[t + 1] - hb->trace_offsets[t];
+            if (k > maxlen) maxlen = k;
+        }
+        if (maxlen < SS_BULK_MIN_DEFAULT) pp.bulk_min = -1;
+    }
+    params = &pp;
     size_t total = in_b + out_b + log_b + ws_b;
     std::lock_guard<std::mutex> lk(g_stage.mu);
     cudaStream_t st = (cudaStream_t)stream;

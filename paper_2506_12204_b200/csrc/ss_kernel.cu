@@ -742,9 +742,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             }
             // stale entries are transient: once none is left the trace returns to
             // the exact fast paths (checked every 32 rounds while flagged)
+#ifndef SS_NO_ANOM_EXIT
             if (uni(anom && (T.rounds & 31) == 0) &&
                 !queue_has_stale<POL>(&A, sm, T.off, T.nF, T.nB, T.nO))
                 anom = false;
+#endif
             // ---- fast path: a stretch of same-batch decode rounds --------------
             // 99.5% of config-B rounds (96% under config D's tight memory) keep the
             // batch equal to the ongoing set: p* is an ongoing (decoding) request,

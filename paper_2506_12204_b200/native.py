@@ -68,9 +68,30 @@ EXPORTED = ("ss_last_error", "ss_device_info", "ss_workspace_bytes", "ss_run_tra
 # detect, eoff scan, init, bulk keys, histogram, plan, 16 x (count, scan,
 # scatter), final copy, sched_kernel. The bulk stages exit at once when no
 # trace admits a bulk group.
-def launches_per_run(params=None) -> int:
+def launches_per_run(params=None, max_trace_len=None) -> int:
     bulk = params is None or params.bulk_min >= 0
+    if params is not None and max_trace_len is not None:
+        bulk = _bulk_possible(params, max_trace_len)
     return 3 + (3 + 16 * 3 + 1 if bulk else 0) + 1
+
+
+def _bulk_possible(params, max_trace_len: int) -> bool:
+    """Whether any trace could admit a bulk group (ss_params.bulk_min)."""
+    if params.bulk_min < 0:
+        return False
+    thr = params.bulk_min if params.bulk_min > 0 else A.SS_BULK_MIN_DEFAULT
+    return max_trace_len >= thr
+
+
+def _with_bulk(params, max_trace_len):
+    """A copy of params with the bulk-sort stage disabled when no trace is long
+    enough to need it (saves its 52 empty launches; results are identical)."""
+    if max_trace_len is None or _bulk_possible(params, max_trace_len) or params.bulk_min < 0:
+        return params
+    q = A.ss_params()
+    C.pointer(q)[0] = params
+    q.bulk_min = -1
+    return q
 
 
 def last_timings():
@@ -170,6 +191,7 @@ class DeviceBatch:
         self.batch = batch
         self.n_traces = batch.n_traces
         self.n_requests = batch.n_requests
+        self.max_trace_len = int(np.diff(batch.offsets).max()) if batch.n_traces else 0
         self.t = {"offsets": torch.from_numpy(np.ascontiguousarray(batch.offsets)).to(device)}
         for f, _ in self.FIELDS:
             self.t[f] = torch.from_numpy(np.ascontiguousarray(getattr(batch, f))).to(device)
@@ -183,6 +205,7 @@ class DeviceBatch:
         self = cls.__new__(cls)
         self.batch = None
         self.n_traces = n_traces
+        self.max_trace_len = per_trace
         n = n_traces * per_trace
         self.n_requests = n
         dts = {"ready": torch.float64, "arrival": torch.float64, "prompt": torch.int32, "true_out": torch.int32,
@@ -250,6 +273,7 @@ def run_device(params, dbatch: DeviceBatch, douts: DeviceOutputs, ws: Workspace,
     import torch
 
     params.flags &= ~A.SS_FLAG_ROUND_LOG
+    params = _with_bulk(params, getattr(dbatch, "max_trace_len", None))
     s = stream if stream is not None else torch.cuda.current_stream()
     ms = C.c_float(0.0)
     db, do = dbatch.struct(), douts.struct()
