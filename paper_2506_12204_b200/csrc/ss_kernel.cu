@@ -786,9 +786,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     for (;;) {
                         // one vote for every exit: a completion, an admission due, p*
                         // queued (no ongoing key below the queue front), round cap / log
-                        const bool other = left <= 0 || T.next_ready <= ss::add(T.clock, 1e-12) ||
-                                           T.rounds >= round_cap || (logging && c.logpos > c.logcap);
-                        if (__all_sync(FULL, other || !(act && klt(okey, F0)))) break;
+                        const bool other = (left <= 0) | (T.next_ready <= ss::add(T.clock, 1e-12)) |
+                                           (T.rounds >= round_cap) | (logging && c.logpos > c.logcap);
+                        if (__all_sync(FULL, other | !(act & klt_nb(okey, F0)))) break;
                         if (uni(T.used > safe_used)) {
                             long long e = (long long)m_mid(mem) - (long long)mem.dec;
                             long long dem = e > 1 ? e : 1;
@@ -796,7 +796,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             if (__any_sync(FULL, act && dem + lane + T.used > cap)) break;  // eviction
                         }
                         double part;  // batch_duration (engine.py:126-149) of an all-decode batch
-                        if (uni(!sum_mode)) {
+                        if (!sum_mode) {  // a kernel parameter: uniform by construction
                             part = decode_step_time((long long)nmax, 1, P);
                         } else {
                             const double st = act ? decode_step_time((long long)m_prompt(mem) + mem.dec + 1, 1, P) : 0.0;
@@ -817,10 +817,12 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         if (want_digest) {
                             const unsigned long long r64 = (unsigned long long)T.rounds;
                             const bool hl = lane >= 29;
-                            const unsigned long long val =
-                                act ? (unsigned long long)mem.slot
-                                    : (lane == 31 ? ss_hdr_word(SS_KIND_DECODE, m, 0, 0)
-                                                  : (lane == 30 ? (unsigned long long)T.used : dbits(end)));
+                            // branch-free role select: grant slot / header / memory / time
+                            const unsigned long long hv = ss_hdr_word(SS_KIND_DECODE, m, 0, 0);
+                            const unsigned long long mv = (unsigned long long)T.used, tv = dbits(end);
+                            unsigned long long val = (lane == 30) ? mv : tv;
+                            val = (lane == 31) ? hv : val;
+                            val = act ? (unsigned long long)mem.slot : val;
                             // ss_term(r, tag, idx, val) with ((r << 24) ^ c) * G = r * (G << 24) + c * G
                             // (c < 2^24): the round part advances by one add per round
                             const unsigned long long term = ss_mix64(val ^ (dgr + dgc));
@@ -863,7 +865,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         Key nx;  // order check needs the next lane's (hi, lo) only
                         nx.hi = __shfl_down_sync(FULL, okey.hi, 1);
                         nx.lo = __shfl_down_sync(FULL, okey.lo, 1);
-                        if (__ballot_sync(FULL, lane + 1 < m && klt(nx, okey))) {
+                        if (__ballot_sync(FULL, (lane + 1 < m) & klt_nb(nx, okey))) {
                             if (act) sm->X[32 + lane] = okey;
                             __syncwarp();
                             int r = 0;
