@@ -777,6 +777,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     // and prefill(0) are the same constants every round
                     const double z0 = ss::add(reload_time(0, P), prefill_time(0, P));
                     const bool sum_mode = A.P.decode_cost_sum != 0;
+                    const bool wide = uni(m > 29);  // header lanes are members too (b > 29)
                     // digest: this lane's term tag and position, pre-multiplied (see ss_term)
                     constexpr unsigned long long DG = 0x9E3779B97F4A7C15ull, DG24 = DG << 24;
                     const uint32_t dtag = act ? SS_TAG_GRANT : (lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME));
@@ -828,12 +829,12 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             const unsigned long long term = ss_mix64(val ^ (dgr + dgc));
                             dgr += DG24;
                             dig += (act || hl) ? term : 0ull;
-                            if (m > 29 && hl && act) {
+                            if (wide) {  // lanes 29..31 are members: header terms in a second pass
                                 const uint32_t htag = lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME);
-                                const unsigned long long hval =
-                                    lane == 31 ? ss_hdr_word(SS_KIND_DECODE, m, 0, 0)
-                                               : (lane == 30 ? (unsigned long long)T.used : dbits(end));
-                                dig += ss_term(r64, htag, 0, hval);
+                                unsigned long long hval = (lane == 30) ? mv : tv;
+                                hval = (lane == 31) ? hv : hval;
+                                const unsigned long long t2 = ss_term(r64, htag, 0, hval);
+                                dig += (hl & act) ? t2 : 0ull;
                             }
                         }
                         if (logging) {
