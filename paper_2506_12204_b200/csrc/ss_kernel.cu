@@ -760,36 +760,51 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 const bool cdec = lane < nc0 && (sm->F[lane].aux & DEC_BIT);
                 if (!__any_sync(FULL, cdec)) {
                     const Key F0 = T.nF > 0 ? sm->F[0] : kinf();
-                    const int m = T.nO;
-                    const bool act = lane < m;
+                    int m = T.nO;
+                    bool act = lane < m;
                     MemS mem;
                     if (act) mem = sm->OM[lane];
-                    // rounds before the first completion (a lane completes when dec + 1 >= tout)
-                    int left = __reduce_min_sync(FULL, act ? (int)(m_tout(mem) - mem.dec) - 1 : 0x7fffffff);
-                    unsigned nmax = __reduce_max_sync(FULL, act ? m_prompt(mem) + mem.dec + 1u : 0u);
-                    // KV admission (engine.py:296-327) of an all-decode batch: immediate 1,
-                    // exclusive scan = lane, demand = max(est, 1) with est non-increasing
-                    // over the stretch; below safe_used no member can need an eviction
-                    long long est0 = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
-                    const int maxdem = (int)__reduce_max_sync(FULL, (unsigned)(est0 > 1 ? est0 : 1));
-                    const long long safe_used = cap - (long long)maxdem - m;
                     // remaining_time of a decoding member (costs.py:174-191): reload(0)
                     // and prefill(0) are the same constants every round
                     const double z0 = ss::add(reload_time(0, P), prefill_time(0, P));
                     const bool sum_mode = A.P.decode_cost_sum != 0;
-                    const bool wide = uni(m > 29);  // header lanes are members too (b > 29)
-                    // digest: this lane's term tag and position, pre-multiplied (see ss_term)
                     constexpr unsigned long long DG = 0x9E3779B97F4A7C15ull, DG24 = DG << 24;
-                    const uint32_t dtag = act ? SS_TAG_GRANT : (lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME));
-                    const unsigned long long dgc = ((((unsigned long long)dtag) << 20) ^ (unsigned long long)(act ? lane : 0)) * DG;
                     unsigned long long dgr = (unsigned long long)T.rounds * DG24;
+                    // per-membership values, recomputed when members complete
+                    int left;                 // rounds before the first completion (dec + 1 >= tout)
+                    unsigned nmax;            // longest context + 1 (decode step of the batch)
+                    long long safe_used;      // no member needs an eviction while used <= this
+                    bool wide;                // header lanes are members too (b > 29)
+                    unsigned long long dgc;   // this lane's digest tag / position, pre-multiplied (ss_term)
+                    auto setup = [&]() {
+                        left = __reduce_min_sync(FULL, act ? (int)(m_tout(mem) - mem.dec) - 1 : 0x7fffffff);
+                        nmax = __reduce_max_sync(FULL, act ? m_prompt(mem) + mem.dec + 1u : 0u);
+                        // KV admission (engine.py:296-327) of an all-decode batch: immediate 1,
+                        // exclusive scan = lane, demand = max(est, 1), est non-increasing
+                        const long long est0 = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
+                        const int maxdem = (int)__reduce_max_sync(FULL, (unsigned)(est0 > 1 ? est0 : 1));
+                        safe_used = cap - (long long)maxdem - m;
+                        wide = uni(m > 29);
+                        const uint32_t dtag =
+                            act ? SS_TAG_GRANT : (lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME));
+                        dgc = ((((unsigned long long)dtag) << 20) ^ (unsigned long long)(act ? lane : 0)) * DG;
+                    };
+                    setup();
                     int k = 0;
+                    long long spool = 0, sgr = 0;  // live and granted requests summed over the rounds
+                    int live_s = live;
                     for (;;) {
                         // one vote for every exit: a completion, an admission due, p*
                         // queued (no ongoing key below the queue front), round cap / log
-                        const bool other = (left <= 0) | (T.next_ready <= ss::add(T.clock, 1e-12)) |
-                                           (T.rounds >= round_cap) | (logging && c.logpos > c.logcap);
-                        if (__all_sync(FULL, other | !(act & klt_nb(okey, F0)))) break;
+                        const bool adm = T.next_ready <= ss::add(T.clock, 1e-12);
+                        const bool capx = (T.rounds >= round_cap) | (logging && c.logpos > c.logcap);
+                        const bool pdec = act & klt_nb(okey, F0);
+                        bool cround = false;  // a member completes in this round
+                        if (__all_sync(FULL, (left <= 0) | adm | capx | !pdec)) {
+                            // completing members are handled here when that is the only reason
+                            if (!uni((left <= 0) & !adm & !capx) || !__any_sync(FULL, pdec)) break;
+                            cround = true;
+                        }
                         if (uni(T.used > safe_used)) {
                             long long e = (long long)m_mid(mem) - (long long)mem.dec;
                             long long dem = e > 1 ? e : 1;
@@ -814,12 +829,29 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             if (lft < 1) lft = 1;
                             mem.ft = ss::add(z0, decode_total_time((long long)m_prompt(mem) + mem.dec, lft, P));
                         }
-                        T.used += m;
+                        unsigned cdm = 0;  // completing lanes (cround only)
+                        if (!cround) {
+                            T.used += m;
+                        } else {
+                            // _complete (engine.py:414-421): finish = end, KV released
+                            const bool done = act & (mem.dec >= m_tout(mem));
+                            cdm = __ballot_sync(FULL, done);
+                            const int delta = act ? (done ? 1 - (int)(m_prompt(mem) + mem.dec) : 1) : 0;
+                            T.used += (long long)__reduce_add_sync(FULL, delta);
+                            if (done) {
+                                mem.ft = 0.0;
+                                mem.flg = (mem.flg & ~F_STAGE) | ST_DONE;
+                                const long long g = T.off + mem.slot;
+                                A.out.req.finish_time[g] = end;
+                                store_dyn(A, g, mem.ft, mem.dec, mem.flg);
+                            }
+                        }
+                        const int ncd = __popc(cdm);
                         if (want_digest) {
                             const unsigned long long r64 = (unsigned long long)T.rounds;
                             const bool hl = lane >= 29;
                             // branch-free role select: grant slot / header / memory / time
-                            const unsigned long long hv = ss_hdr_word(SS_KIND_DECODE, m, 0, 0);
+                            const unsigned long long hv = ss_hdr_word(SS_KIND_DECODE, m, ncd, 0);
                             const unsigned long long mv = (unsigned long long)T.used, tv = dbits(end);
                             unsigned long long val = (lane == 30) ? mv : tv;
                             val = (lane == 31) ? hv : val;
@@ -827,7 +859,6 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             // ss_term(r, tag, idx, val) with ((r << 24) ^ c) * G = r * (G << 24) + c * G
                             // (c < 2^24): the round part advances by one add per round
                             const unsigned long long term = ss_mix64(val ^ (dgr + dgc));
-                            dgr += DG24;
                             dig += (act || hl) ? term : 0ull;
                             if (wide) {  // lanes 29..31 are members: header terms in a second pass
                                 const uint32_t htag = lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME);
@@ -836,22 +867,26 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                 const unsigned long long t2 = ss_term(r64, htag, 0, hval);
                                 dig += (hl & act) ? t2 : 0ull;
                             }
+                            if (cround && ((cdm >> lane) & 1u))
+                                dig += ss_term(r64, SS_TAG_DONE, __popc(cdm & lt), mem.slot);
                         }
+                        dgr += DG24;
                         if (logging) {
                             const long long lp = c.logpos;
                             if (act) log_put(c, lp + SS_LOG_HEADER_WORDS + lane, mem.slot);
+                            if ((cdm >> lane) & 1u) log_put(c, lp + SS_LOG_HEADER_WORDS + m + __popc(cdm & lt), mem.slot);
                             __syncwarp();
                             if (lane == 0) {
                                 const unsigned long long mu = (unsigned long long)T.used, tb = dbits(end);
                                 log_put(c, lp + 0, (uint32_t)SS_KIND_DECODE);
                                 log_put(c, lp + 1, (uint32_t)m);
-                                log_put(c, lp + 2, 0u);
+                                log_put(c, lp + 2, (uint32_t)ncd);
                                 log_put(c, lp + 3, 0u);
                                 log_put(c, lp + 4, (uint32_t)mu);
                                 log_put(c, lp + 5, (uint32_t)(mu >> 32));
                                 log_put(c, lp + 6, (uint32_t)tb);
                                 log_put(c, lp + 7, (uint32_t)(tb >> 32));
-                                c.logpos = lp + SS_LOG_HEADER_WORDS + m;
+                                c.logpos = lp + SS_LOG_HEADER_WORDS + m + ncd;
                             }
                             __syncwarp();
                         }
@@ -861,6 +896,39 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         nmax += 1u;
                         left -= 1;
                         k += 1;
+                        spool += live_s;
+                        sgr += m;
+                        if (cround) {
+                            // resident list upkeep for the completed (engine.py:414-421)
+                            unsigned cm = cdm;
+                            __syncwarp();
+                            while (cm) {
+                                const int q = __ffs(cm) - 1;
+                                cm &= cm - 1;
+                                const uint32_t s = __shfl_sync(FULL, mem.slot, q);
+                                if (lane == 0) {
+                                    const uint32_t ri = A.w.rpos[T.off + s];
+                                    const uint32_t last = A.w.R[T.off + T.nR - 1];
+                                    A.w.R[T.off + ri] = last;
+                                    A.w.rpos[T.off + last] = ri;
+                                }
+                                T.nR -= 1;
+                                __syncwarp();
+                            }
+                            // ongoing = granted members not completed, in granted order
+                            const bool stay = act & !((cdm >> lane) & 1u);
+                            const unsigned smk = __ballot_sync(FULL, stay);
+                            if (stay) sm->OM[__popc(smk & lt)] = mem;
+                            __syncwarp();
+                            m = __popc(smk);
+                            act = lane < m;
+                            if (act) mem = sm->OM[lane];
+                            __syncwarp();
+                            T.nO = m;
+                            live_s -= ncd;
+                            if (uni(m == 0)) break;
+                            setup();
+                        }
                         // the ongoing set stays sorted by key (usually already is)
                         okey = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, true);
                         Key nx;  // order check needs the next lane's (hi, lo) only
@@ -892,9 +960,10 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             sm->OM[lane] = mem;
                             sm->X[32 + lane] = okey;
                         }
+                        T.nO = m;
                         if (lane == 0) {
-                            c.s_pool += (long long)live * k;
-                            c.s_granted += (long long)m * k;
+                            c.s_pool += spool;
+                            c.s_granted += sgr;
                         }
                         __syncwarp();
                         continue;
