@@ -496,7 +496,8 @@ def main():
             t1 = time.perf_counter()
             rc = L.ss_run_traces_host(C.byref(pf()), C.byref(hb), C.byref(o), st, None)
             et.append(time.perf_counter() - t1)
-            assert rc == 0, native.last_error()
+            # traces the reference itself fails on report SS_ERR_TRACE_FAILED (stats carry them)
+            assert rc in (A.SS_OK, A.SS_ERR_TRACE_FAILED), native.last_error()
         e_tot = torch.tensor([sum(et)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_tot, op=dist.ReduceOp.MAX)
