@@ -197,7 +197,12 @@ typedef struct ss_outputs {
 /* ---- schedule digest -------------------------------------------------
  * Order-sensitive and lane-parallel: a sum (mod 2^64) of one hashed term per
  * (round, field, position). Shared verbatim by the oracle (tests) and the
- * device so full-size parity reduces to comparing one u64 per trace. */
+ * device so full-size parity reduces to comparing one u64 per trace.
+ * The granted list of round r contributes
+ *     ss_round_mul(r) * sum_pos ss_grant_term(pos, slot_pos)      (mod 2^64)
+ * (an odd round multiplier times a position-tagged hash of the list), so a
+ * batch that stays the same over a stretch of rounds hashes once; every other
+ * field is one ss_term(round, tag, index, value). */
 #if defined(__CUDACC__)
 #define SS_HD __host__ __device__ __forceinline__
 #else
@@ -212,10 +217,16 @@ SS_HD uint64_t ss_mix64(uint64_t z) {
 SS_HD uint64_t ss_term(uint64_t round, uint32_t tag, uint32_t idx, uint64_t v) {
     return ss_mix64(v ^ (((round << 24) ^ ((uint64_t)tag << 20) ^ (uint64_t)idx) * 0x9E3779B97F4A7C15ull));
 }
+#define SS_DG_POS   0xD6E8FEB86659FD93ull
+#define SS_DG_ROUND 0xA0761D6478BD642Full
+SS_HD uint64_t ss_grant_term(uint32_t pos, uint64_t slot) {
+    return ss_mix64(slot ^ ((uint64_t)(pos + 1u) * SS_DG_POS));
+}
+SS_HD uint64_t ss_round_mul(uint64_t round) { return (2u * round + 1u) * SS_DG_ROUND; }
 #define SS_TAG_HDR   1u
 #define SS_TAG_MEM   2u
 #define SS_TAG_TIME  3u
-#define SS_TAG_GRANT 4u
+#define SS_TAG_GRANT 4u   /* unused since the grant terms above */
 #define SS_TAG_DONE  5u
 #define SS_TAG_EV0   6u   /* victim | action<<32     */
 #define SS_TAG_EV1   7u   /* saved | discarded<<32   */

@@ -461,7 +461,9 @@ static void record_round(osim* s, int kind, const int* g, int m, const int* c, i
         d += ss_term(r, SS_TAG_MEM, 0, (uint64_t)s->used);
         uint64_t tb; memcpy(&tb, &t, 8);
         d += ss_term(r, SS_TAG_TIME, 0, tb);
-        for (int j = 0; j < m; j++) d += ss_term(r, SS_TAG_GRANT, j, (uint64_t)g[j]);
+        uint64_t gh = 0;
+        for (int j = 0; j < m; j++) gh += ss_grant_term((uint32_t)j, (uint64_t)g[j]);
+        d += gh * ss_round_mul(r);
         for (int j = 0; j < nc; j++) d += ss_term(r, SS_TAG_DONE, j, (uint64_t)c[j]);
         for (int k = 0; k < v; k++) {
             odecision* e = &s->dec[k];

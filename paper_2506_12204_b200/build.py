@@ -11,6 +11,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import tempfile
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
@@ -45,9 +46,10 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     if not force and not _stale() and out is None:
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
+    objdir = LIBDIR if out is None else tempfile.mkdtemp(prefix="ss_build_")  # variants build in parallel
     objs = []
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + ".o")
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         if src.endswith(".cpp"):
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread",
                    "-c", os.path.join(CSRC, src), "-o", obj]

@@ -45,6 +45,13 @@ SS_HDI double decode_total_time(int64_t n, int64_t m, const ss_profile& p) {
     inner = add(inner, mul(0.5, dm));
     return add(mul(p.gamma1, inner), mul(p.gamma2, dm));
 }
+// the same value for 32-bit token counts (n*m < 2^64 exactly; conversions exact-rounded alike)
+SS_HDI double decode_total_time_u32(uint32_t n, uint32_t m, const ss_profile& p) {
+    double dm = (double)m;
+    double inner = add(mul(mul(0.5, dm), dm), (double)((unsigned long long)n * m));
+    inner = add(inner, mul(0.5, dm));
+    return add(mul(p.gamma1, inner), mul(p.gamma2, dm));
+}
 // costs.py:119-122
 SS_HDI double reload_time(int64_t tokens, const ss_profile& p) {
     return mul(p.beta_load, (double)tokens);

@@ -44,6 +44,9 @@
 #ifndef SS_MINB
 #define SS_MINB 4  // min resident CTAs per SM requested from ptxas (register cap: 128)
 #endif
+#ifndef SS_CHUNK_MIN
+#define SS_CHUNK_MIN 4  // shortest static bound for which a stretch runs a lane-per-round chunk
+#endif
 
 namespace ss {
 
@@ -572,6 +575,25 @@ __device__ __noinline__ bool queue_has_stale(const KArgs* Ap, const WarpSmem* sm
     return __any_sync(FULL, st);
 }
 
+// ---- SS_DEBUG_TIMING builds: warp-cycles per kernel section -----------------
+#ifdef SS_DEBUG_TIMING
+__device__ unsigned long long g_dbg_cycles[16];
+#define SS_SECT(s_)                                                   \
+    do {                                                              \
+        const long long now_ = clock64();                             \
+        dbg_acc[dbg_cur] += (unsigned long long)(now_ - dbg_t);       \
+        dbg_t = now_;                                                 \
+        dbg_cur = (s_);                                               \
+    } while (0)
+#define SS_DCOUNT(k_, v_) (dbg_acc[8 + (k_)] += (unsigned long long)(v_))
+#else
+#define SS_SECT(s_) ((void)0)
+#define SS_DCOUNT(k_, v_) ((void)0)
+#endif
+// sections: 0 init/admission/top, 1 fast path per-round body, 2 chunk, 3 general round, 4 outputs,
+// 5 stretch entry, 6 stretch round vote, 7 stretch order check
+// counters: 8 chunks, 9 chunk rounds, 10 per-round fast rounds, 11 general rounds
+
 // ---- per-lane member quantities (32-bit: token counts of one request) -------
 struct MemQ {
     bool isdec;
@@ -609,6 +631,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
     const unsigned lt = lanemask_lt();
     constexpr bool want_digest = (MODE & 1) != 0;
     constexpr bool logging = (MODE & 2) != 0;
+#ifdef SS_DEBUG_TIMING
+    unsigned long long dbg_acc[16] = {0};
+    long long dbg_t = clock64();
+    int dbg_cur = 0;
+#endif
 
     for (;;) {
         int t = 0;
@@ -684,6 +711,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
 
         // ---- the round loop (engine.py:202-224)
         while (uni(T.status == SS_TRACE_OK)) {
+            SS_SECT(0);
             // admission of prediction-ready requests (engine.py:204-206)
             const double thr = ss::add(T.clock, 1e-12);
             if (uni(T.next_ready <= thr)) {
@@ -756,6 +784,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             // the same arithmetic, digest terms and bookkeeping as the general
             // round below (engine.py:288-380), which handles every other round.
             if (POL == SS_POLICY_SEMANTIC && uni(!anom && T.nO > 0 && T.nO <= b)) {
+                SS_SECT(5);
                 const int nc0 = T.nF < b ? T.nF : b;
                 const bool cdec = lane < nc0 && (sm->F[lane].aux & DEC_BIT);
                 if (!__any_sync(FULL, cdec)) {
@@ -774,8 +803,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     int left;                 // rounds before the first completion (dec + 1 >= tout)
                     unsigned nmax;            // longest context + 1 (decode step of the batch)
                     long long safe_used;      // no member needs an eviction while used <= this
-                    bool wide;                // header lanes are members too (b > 29)
-                    unsigned long long dgc;   // this lane's digest tag / position, pre-multiplied (ss_term)
+                    unsigned long long gt;    // this lane's grant term (ss_grant_term of its batch position)
+                    // header lanes 29..31: tag pre-multiplied (ss_term); round multiplier of the grant terms
+                    const unsigned long long dgc =
+                        ((unsigned long long)(lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME)) << 20) * DG;
+                    unsigned long long rmul = ss_round_mul((unsigned long long)T.rounds);
                     auto setup = [&]() {
                         left = __reduce_min_sync(FULL, act ? (int)(m_tout(mem) - mem.dec) - 1 : 0x7fffffff);
                         nmax = __reduce_max_sync(FULL, act ? m_prompt(mem) + mem.dec + 1u : 0u);
@@ -784,16 +816,14 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         const long long est0 = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
                         const int maxdem = (int)__reduce_max_sync(FULL, (unsigned)(est0 > 1 ? est0 : 1));
                         safe_used = cap - (long long)maxdem - m;
-                        wide = uni(m > 29);
-                        const uint32_t dtag =
-                            act ? SS_TAG_GRANT : (lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME));
-                        dgc = ((((unsigned long long)dtag) << 20) ^ (unsigned long long)(act ? lane : 0)) * DG;
+                        gt = act ? ss_grant_term((uint32_t)lane, mem.slot) : 0ull;
                     };
                     setup();
                     int k = 0;
                     long long spool = 0, sgr = 0;  // live and granted requests summed over the rounds
                     int live_s = live;
                     for (;;) {
+                        SS_SECT(6);
                         // one vote for every exit: a completion, an admission due, p*
                         // queued (no ongoing key below the queue front), round cap / log
                         const bool adm = T.next_ready <= ss::add(T.clock, 1e-12);
@@ -811,7 +841,30 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             if (dem + lane > cap) dem = 1;
                             if (__any_sync(FULL, act && dem + lane + T.used > cap)) break;  // eviction
                         }
+                        // ---- a chunk of up to 32 rounds, one lane per round ----------
+                        // Within a stretch nothing but the clock is a serial chain: round
+                        // j's batch duration, the members' keys after j decode steps and
+                        // every digest term are closed-form in j. The clock is summed in
+                        // the reference's order (one add per round); lane j evaluates
+                        // round j. The chunk ends before the first round that the per-round
+                        // exit vote would refuse (admission due, p* queued, ongoing order
+                        // changed, completion, round cap, memory or log bound).
+                        // entry: the static bounds (completion, round cap, memory, log) allow
+                        // at least SS_CHUNK_MIN rounds; per-round bounds are lane votes below
+                        bool chunk = false;
+#ifndef SS_NO_CHUNK
+                        if (!cround && !sum_mode) {
+                            chunk = left >= SS_CHUNK_MIN && T.rounds + (SS_CHUNK_MIN - 1) < round_cap &&
+                                    T.used + (long long)(SS_CHUNK_MIN - 1) * m <= safe_used;
+                            if (logging)
+                                chunk = chunk && c.logpos + (long long)(SS_CHUNK_MIN - 1) * (SS_LOG_HEADER_WORDS + m) <=
+                                                     c.logcap;
+                        }
+#endif
+                        if (uni(!chunk)) {  // one round here; the chunk below is laid out after the loop's hot path
                         double part;  // batch_duration (engine.py:126-149) of an all-decode batch
+                        SS_SECT(1);
+                        SS_DCOUNT(2, 1);
                         if (!sum_mode) {  // a kernel parameter: uniform by construction
                             part = decode_step_time((long long)nmax, 1, P);
                         } else {
@@ -850,27 +903,22 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         if (want_digest) {
                             const unsigned long long r64 = (unsigned long long)T.rounds;
                             const bool hl = lane >= 29;
-                            // branch-free role select: grant slot / header / memory / time
+                            // header / memory / time terms in lanes 29..31 (branch-free role select);
+                            // the members' cached grant terms times this round's multiplier
                             const unsigned long long hv = ss_hdr_word(SS_KIND_DECODE, m, ncd, 0);
                             const unsigned long long mv = (unsigned long long)T.used, tv = dbits(end);
                             unsigned long long val = (lane == 30) ? mv : tv;
                             val = (lane == 31) ? hv : val;
-                            val = act ? (unsigned long long)mem.slot : val;
-                            // ss_term(r, tag, idx, val) with ((r << 24) ^ c) * G = r * (G << 24) + c * G
+                            // ss_term(r, tag, 0, val) with ((r << 24) ^ c) * G = r * (G << 24) + c * G
                             // (c < 2^24): the round part advances by one add per round
                             const unsigned long long term = ss_mix64(val ^ (dgr + dgc));
-                            dig += (act || hl) ? term : 0ull;
-                            if (wide) {  // lanes 29..31 are members: header terms in a second pass
-                                const uint32_t htag = lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME);
-                                unsigned long long hval = (lane == 30) ? mv : tv;
-                                hval = (lane == 31) ? hv : hval;
-                                const unsigned long long t2 = ss_term(r64, htag, 0, hval);
-                                dig += (hl & act) ? t2 : 0ull;
-                            }
+                            dig += hl ? term : 0ull;
+                            dig += act ? gt * rmul : 0ull;
                             if (cround && ((cdm >> lane) & 1u))
                                 dig += ss_term(r64, SS_TAG_DONE, __popc(cdm & lt), mem.slot);
                         }
                         dgr += DG24;
+                        rmul += 2u * SS_DG_ROUND;
                         if (logging) {
                             const long long lp = c.logpos;
                             if (act) log_put(c, lp + SS_LOG_HEADER_WORDS + lane, mem.slot);
@@ -929,12 +977,14 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             if (uni(m == 0)) break;
                             setup();
                         }
+                        SS_SECT(7);
                         // the ongoing set stays sorted by key (usually already is)
                         okey = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, true);
                         Key nx;  // order check needs the next lane's (hi, lo) only
                         nx.hi = __shfl_down_sync(FULL, okey.hi, 1);
                         nx.lo = __shfl_down_sync(FULL, okey.lo, 1);
-                        if (__ballot_sync(FULL, (lane + 1 < m) & klt_nb(nx, okey))) {
+                        const bool reord = uni(__ballot_sync(FULL, (lane + 1 < m) & klt_nb(nx, okey)) != 0u);
+                        if (reord) {
                             if (act) sm->X[32 + lane] = okey;
                             __syncwarp();
                             int r = 0;
@@ -951,6 +1001,134 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             }
                             __syncwarp();
                         }
+                        if (reord) break;  // positions moved: the next stretch recomputes the grant terms
+                            continue;
+                        }
+#ifndef SS_NO_CHUNK
+                        {
+                            SS_SECT(2);
+                            const int L = left < 32 ? left : 32;
+                            if (act) sm->OM[lane] = mem;  // broadcast source of the member loop
+                            double* chain = reinterpret_cast<double*>(sm->M);  // round ends (scratch)
+                            // batch_duration of round j: decode step at the longest context
+                            const double pj =
+                                ss::add(0.0, decode_step_time((long long)(nmax + (unsigned)lane), 1, P));
+                            double clk = T.clock;
+                            for (int q0 = 0; uni(q0 < L); q0 += 8) {
+#pragma unroll
+                                for (int q = 0; q < 8; q++) {
+                                    clk = ss::add(clk, __shfl_sync(FULL, pj, q0 + q));
+                                    if (lane == 0) chain[q0 + q] = clk;
+                                }
+                            }
+                            __syncwarp();
+                            const double endj = chain[lane];
+                            const double befj = lane == 0 ? T.clock : chain[lane - 1];
+                            // state after round j (lane j): every member decoded j + 1 more
+                            const uint32_t dj = (uint32_t)lane + 1u;
+                            const unsigned long long rj = (unsigned long long)(T.rounds + lane);
+                            bool ok = true, pk = true;
+                            double pft = 0.0;
+                            uint32_t prk = 0, ptie = 0;
+                            for (int i = 0; uni(i < m); i++) {
+                                const uint4 st = sm->OM[i].st;
+                                const uint32_t dec = sm->OM[i].dec + dj;
+                                int lft = (int)st.z - (int)dec;
+                                lft = lft < 1 ? 1 : lft;
+                                const double ft = ss::add(z0, decode_total_time_u32(st.x + dec, (uint32_t)lft, P));
+                                const uint32_t rk = st.w >> 24, tie = st.w & SLOT_MASK;
+                                // key order (rank, f_t, tie) without packing: f_t > 0 orders like its bits
+                                if (i == 0) pk = klt_nb(make_key<POL>(rk, ft, tie, 0, true), F0);
+                                else ok &= (prk < rk) | ((prk == rk) & ((pft < ft) | ((pft == ft) & (ptie < tie))));
+                                pft = ft;
+                                prk = rk;
+                                ptie = tie;
+                            }
+                            // round j runs iff rounds 0..j-1 left the members sorted with p*
+                            // ongoing, no admission is due at its start and no static bound
+                            // (completion, round cap, memory safety, log space) stops it
+                            const bool adm_j = T.next_ready <= ss::add(befj, 1e-12);
+                            bool lim = (lane >= L) | (T.rounds + lane >= round_cap) |
+                                       (T.used + (long long)lane * m > safe_used);
+                            if (logging) lim |= c.logpos + (long long)lane * (SS_LOG_HEADER_WORDS + m) > c.logcap;
+                            const unsigned stop = __ballot_sync(FULL, lim | adm_j) |
+                                                  (__ballot_sync(FULL, !(pk & ok)) << 1);
+                            const int Lx = stop ? __ffs(stop) - 1 : 32;  // >= 1: round 0 passed the vote
+                            SS_DCOUNT(0, 1);
+                            SS_DCOUNT(1, Lx);
+                            const bool runj = lane < Lx;
+                            const long long used_j = T.used + (long long)(lane + 1) * m;
+                            if (want_digest) {
+                                const unsigned long long hv = ss_hdr_word(SS_KIND_DECODE, m, 0, 0);
+                                const unsigned long long tr = ss_term(rj, SS_TAG_HDR, 0, hv) +
+                                                              ss_term(rj, SS_TAG_MEM, 0, (unsigned long long)used_j) +
+                                                              ss_term(rj, SS_TAG_TIME, 0, dbits(endj));
+                                // the batch list hashes once: sum of the members' grant terms
+                                const unsigned long long hb = warp_sum_u64(gt);
+                                dig += runj ? hb * ss_round_mul(rj) + tr : 0ull;
+                            }
+                            if (logging) {
+                                __syncwarp();
+                                const long long lp = c.logpos + (long long)lane * (SS_LOG_HEADER_WORDS + m);
+                                if (runj) {
+                                    const unsigned long long mu = (unsigned long long)used_j, tb = dbits(endj);
+                                    log_put(c, lp + 0, (uint32_t)SS_KIND_DECODE);
+                                    log_put(c, lp + 1, (uint32_t)m);
+                                    log_put(c, lp + 2, 0u);
+                                    log_put(c, lp + 3, 0u);
+                                    log_put(c, lp + 4, (uint32_t)mu);
+                                    log_put(c, lp + 5, (uint32_t)(mu >> 32));
+                                    log_put(c, lp + 6, (uint32_t)tb);
+                                    log_put(c, lp + 7, (uint32_t)(tb >> 32));
+                                    for (int i = 0; i < m; i++) log_put(c, lp + SS_LOG_HEADER_WORDS + i, sm->OM[i].slot);
+                                }
+                                __syncwarp();
+                                if (lane == 0) c.logpos += (long long)Lx * (SS_LOG_HEADER_WORDS + m);
+                                __syncwarp();
+                            }
+                            T.clock = chain[Lx - 1];
+                            __syncwarp();
+                            T.used += (long long)Lx * m;
+                            peak = T.used > peak ? T.used : peak;
+                            T.rounds += Lx;
+                            nmax += (unsigned)Lx;
+                            left -= Lx;
+                            k += Lx;
+                            spool += (long long)Lx * live_s;
+                            sgr += (long long)Lx * m;
+                            dgr += (unsigned long long)Lx * DG24;
+                            rmul += (unsigned long long)Lx * (2u * SS_DG_ROUND);
+                            mem.dec += (uint32_t)Lx;
+                            long long lft = (long long)m_mid(mem) - (long long)mem.dec;
+                            if (lft < 1) lft = 1;
+                            mem.ft = ss::add(z0, decode_total_time((long long)m_prompt(mem) + mem.dec, lft, P));
+                        }
+                        SS_SECT(7);
+                        // the ongoing set stays sorted by key (usually already is)
+                        okey = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, true);
+                        Key nx;  // order check needs the next lane's (hi, lo) only
+                        nx.hi = __shfl_down_sync(FULL, okey.hi, 1);
+                        nx.lo = __shfl_down_sync(FULL, okey.lo, 1);
+                        const bool reord = uni(__ballot_sync(FULL, (lane + 1 < m) & klt_nb(nx, okey)) != 0u);
+                        if (reord) {
+                            if (act) sm->X[32 + lane] = okey;
+                            __syncwarp();
+                            int r = 0;
+                            for (int q = 0; uni(q < m); q++) r += klt(sm->X[32 + q], okey) ? 1 : 0;
+                            __syncwarp();
+                            if (act) {
+                                sm->OM[r] = mem;
+                                sm->X[32 + r] = okey;
+                            }
+                            __syncwarp();
+                            if (act) {
+                                mem = sm->OM[lane];
+                                okey = sm->X[32 + lane];
+                            }
+                            __syncwarp();
+                        }
+                        if (reord) break;  // positions moved: the next stretch recomputes the grant terms
+#endif
                     }
                     if (uni(T.rounds >= round_cap)) set_status(T, SS_TRACE_ROUND_CAP);
                     if (logging && uni(c.logpos > c.logcap)) set_status(T, SS_TRACE_LOG_OVERFLOW);
@@ -971,6 +1149,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 }
             }
             if (lane == 0) c.s_pool += live;
+            SS_SECT(3);
+            SS_DCOUNT(3, 1);
 #ifdef SS_DEBUG_ANOM
             if (lane == 0) c.dbg += anom ? 1 : 0;
 #endif
@@ -1512,8 +1692,12 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     const unsigned long long hval =
                         lane == 31 ? ss_hdr_word(kind, ng, nc_done, R.ndec)
                                    : (lane == 30 ? (unsigned long long)T.used : dbits(end));
-                    if (g_act || hl) {
-                        dig += g_act ? ss_term(r64, SS_TAG_GRANT, gi, mem.slot) : ss_term(r64, htag, 0, hval);
+                    if (g_act || hl) {  // one mix per lane: grant term or ss_term(r, htag, 0, hval)
+                        const unsigned long long x =
+                            g_act ? ((unsigned long long)mem.slot ^ ((unsigned long long)(gi + 1) * SS_DG_POS))
+                                  : (hval ^ (((r64 << 24) ^ ((unsigned long long)htag << 20)) * 0x9E3779B97F4A7C15ull));
+                        const unsigned long long h = ss_mix64(x);
+                        dig += g_act ? h * ss_round_mul(r64) : h;
                     }
                     if (m > 29 && hl && g_act) dig += ss_term(r64, htag, 0, hval);
                     if (cdone && done) dig += ss_term(r64, SS_TAG_DONE, ci, mem.slot);
@@ -1606,6 +1790,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         }
 
         // ---- outputs and the fused statistics (metrics.py:35-56)
+        SS_SECT(4);
         {
             PySum acc;
             acc.init();
@@ -1677,6 +1862,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         }
         __syncwarp();
     }
+#ifdef SS_DEBUG_TIMING
+    SS_SECT(0);
+    if (lane == 0)
+        for (int i = 0; i < 16; i++) atomicAdd(&g_dbg_cycles[i], dbg_acc[i]);
+#endif
 }
 
 // --------------------------------------------------------------------------
@@ -1773,3 +1963,13 @@ int launch_sched(const KArgs& a, int blocks, void* stream) {
 }
 
 }  // namespace ss
+
+#ifdef SS_DEBUG_TIMING
+// debug builds only (not part of include/semsched_b200.h): read and clear the section counters
+extern "C" int ss_debug_cycles(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out, ss::g_dbg_cycles, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+    unsigned long long z[16] = {0};
+    return cudaMemcpyToSymbol(ss::g_dbg_cycles, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -57,6 +57,14 @@ def term(rnd, tag, idx, v):
     return mix64((v & M64) ^ salt)
 
 
+def grant_term(pos, slot):
+    return mix64((slot ^ (((pos + 1) * 0xD6E8FEB86659FD93) & M64)) & M64)
+
+
+def round_mul(rnd):
+    return ((2 * rnd + 1) * 0xA0761D6478BD642F) & M64
+
+
 def fbits(x):
     return struct.unpack("<Q", struct.pack("<d", x))[0]
 
@@ -197,8 +205,10 @@ def run_case(name, cfg, arrivals_fn, keep_log):
         d = term(k, 1, 0, rd["kind"] | (len(g) << 8) | (len(c) << 24) | (len(decs) << 40))
         d += term(k, 2, 0, rd["mem_used"])
         d += term(k, 3, 0, fbits(rd["time"]))
+        gh = 0
         for j, s in enumerate(g):
-            d += term(k, 4, j, s)
+            gh += grant_term(j, s)
+        d += (gh & M64) * round_mul(k)
         for j, s in enumerate(c):
             d += term(k, 5, j, s)
         dl = []
