@@ -70,6 +70,12 @@ extern "C" {
 /* ---- flags ----------------------------------------------------------- */
 #define SS_FLAG_ROUND_LOG  1u   /* write per-round ITERATION_END records     */
 #define SS_FLAG_DIGEST     2u   /* accumulate the per-trace schedule digest   */
+/* Scheduler variant (results are identical; speed differs). By default the run
+ * uses chunked stretches of same-batch decode rounds (32 rounds per warp step)
+ * when no trace's KV footprint bound can reach the budget, else one round per
+ * step. These flags force one variant (tests cover both on every case). */
+#define SS_FLAG_FORCE_CHUNKED  4u
+#define SS_FLAG_FORCE_PERROUND 8u
 
 /* limits of the device path */
 #define SS_MAX_BATCH       32   /* one scheduler candidate per lane of a warp */

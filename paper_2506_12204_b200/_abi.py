@@ -27,6 +27,8 @@ TRACE_STATUS_NAMES = {0: "ok", 1: "livelock", 2: "round_cap", 3: "log_overflow",
 SS_POLICY = {"semantic": 0, "fcfs": 1, "sjf": 2, "hpjf": 3}
 SS_FLAG_ROUND_LOG = 1
 SS_FLAG_DIGEST = 2
+SS_FLAG_FORCE_CHUNKED = 4
+SS_FLAG_FORCE_PERROUND = 8
 SS_MAX_BATCH = 32
 SS_MAX_LEVELS = 16
 SS_MAX_TRACE_REQS = 1 << 24

@@ -631,6 +631,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
     const unsigned lt = lanemask_lt();
     constexpr bool want_digest = (MODE & 1) != 0;
     constexpr bool logging = (MODE & 2) != 0;
+    // MODE bit 2: the chunked-stretch variant. Semantic runs launch both variants
+    // back to back; the one the prepass did not select (ss_prepass.cu
+    // select_kernel: chunks only when the KV budget can never bind) exits at once.
+    constexpr bool chunking = (MODE & 4) != 0;
+    if (POL == SS_POLICY_SEMANTIC && *A.w.sel != (chunking ? 1 : 0)) return;
 #ifdef SS_DEBUG_TIMING
     unsigned long long dbg_acc[16] = {0};
     long long dbg_t = clock64();
@@ -853,7 +858,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         // at least SS_CHUNK_MIN rounds; per-round bounds are lane votes below
                         bool chunk = false;
 #ifndef SS_NO_CHUNK
-                        if (!cround && !sum_mode) {
+                        if (chunking && !cround && !sum_mode) {
                             chunk = left >= SS_CHUNK_MIN && T.rounds + (SS_CHUNK_MIN - 1) < round_cap &&
                                     T.used + (long long)(SS_CHUNK_MIN - 1) * m <= safe_used;
                             if (logging)
@@ -861,7 +866,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                                      c.logcap;
                         }
 #endif
-                        if (uni(!chunk)) {  // one round here; the chunk below is laid out after the loop's hot path
+                        if (!chunking || uni(!chunk)) {  // one round here; the chunk below is laid out after the loop's hot path
                         double part;  // batch_duration (engine.py:126-149) of an all-decode batch
                         SS_SECT(1);
                         SS_DCOUNT(2, 1);
@@ -1879,7 +1884,7 @@ static long long tiles_for(int64_t n) { return ((n > 0 ? n : 1) + RS_TILE - 1) /
 // Layout: zero-initialised block first (one memset per run), then scratch.
 size_t work_bytes(int64_t n, int32_t T) {
     size_t nn = (size_t)(n > 0 ? n : 1), tt = (size_t)(T > 0 ? T : 1);
-    size_t zero = align16(tt * 8) + align16(tt * 4) + align16((size_t)RS_PASSES * 256 * 4) + 16;
+    size_t zero = 2 * align16(tt * 8) + align16(tt * 4) + align16((size_t)RS_PASSES * 256 * 4) + 16;
     // st, dy, B, ins, S: 16 B; rpos, R, pend, tt0, tt1: 4 B
     return zero + 5 * align16(nn * 16) + 5 * align16(nn * 4) + align16(tt * 4) + align16((tt + 1) * 8) +
            align16((size_t)(RS_PASSES + 1) * 4) + align16((size_t)256 * tiles_for(n) * 4);
@@ -1887,16 +1892,17 @@ size_t work_bytes(int64_t n, int32_t T) {
 
 size_t work_zero_bytes(int32_t T) {
     size_t tt = (size_t)(T > 0 ? T : 1);
-    return align16(tt * 8) + align16(tt * 4) + align16((size_t)RS_PASSES * 256 * 4) + 16;
+    return 2 * align16(tt * 8) + align16(tt * 4) + align16((size_t)RS_PASSES * 256 * 4) + 16;
 }
 
 void carve_work(void* base, int64_t n, int32_t T, Work* w) {
     size_t nn = (size_t)(n > 0 ? n : 1), tt = (size_t)(T > 0 ? T : 1);
     char* p = (char*)base;
     w->tok = (unsigned long long*)p; p += align16(tt * 8);
+    w->foot = (unsigned long long*)p; p += align16(tt * 8);
     w->nuns = (uint32_t*)p;  p += align16(tt * 4);
     w->hist = (uint32_t*)p;  p += align16((size_t)RS_PASSES * 256 * 4);
-    w->next_trace = (int*)p; p += 16;
+    w->next_trace = (int*)p; w->sel = (int*)p + 1; p += 16;
     w->st = (void*)p;        p += align16(nn * 16);
     w->dy = (void*)p;        p += align16(nn * 16);
     w->B = (void*)p;         p += align16(nn * 16);
@@ -1926,7 +1932,12 @@ static const void* kernel_ptr(int mode) {
     case 0: return (const void*)sched_kernel<POL, 0>;
     case 1: return (const void*)sched_kernel<POL, 1>;
     case 2: return (const void*)sched_kernel<POL, 2>;
-    default: return (const void*)sched_kernel<POL, 3>;
+    case 3: return (const void*)sched_kernel<POL, 3>;
+    // chunked-stretch variants: the fast path exists for the semantic policy only
+    case 4: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 4> : nullptr;
+    case 5: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 5> : nullptr;
+    case 6: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 6> : nullptr;
+    default: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 7> : nullptr;
     }
 }
 
@@ -1958,9 +1969,16 @@ int launch_sched(const KArgs& a, int blocks, void* stream) {
     const void* k = kernel_for(a.P.policy, mode_of(a.P.flags));
     if (!k) return SS_ERR_UNSUPPORTED;
     void* argv[] = {(void*)&a};
+    if (a.P.policy == SS_POLICY_SEMANTIC) {  // the chunked variant first; the unselected one exits at once
+        const void* kc = kernel_for(a.P.policy, mode_of(a.P.flags) | 4);
+        cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaLaunchKernel(kc, dim3(blocks), dim3(32 * WPB), argv, smem, st) != cudaSuccess) return SS_ERR_CUDA;
+    }
     if (cudaLaunchKernel(k, dim3(blocks), dim3(32 * WPB), argv, smem, st) != cudaSuccess) return SS_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? SS_OK : SS_ERR_CUDA;
 }
+
+int sched_launches(int policy) { return policy == SS_POLICY_SEMANTIC ? 2 : 1; }
 
 }  // namespace ss
 

@@ -23,6 +23,8 @@ struct Work {
     uint32_t* tt0;            // radix sort payload: trace index of each key (ping-pong pair)
     uint32_t* tt1;
     unsigned long long* tok;  // per trace: sum of true output lengths (round cap)
+    unsigned long long* foot; // per trace: sum of prompt + max(true, predicted) output + 1 (KV footprint bound)
+    int* sel;                 // scheduler variant for this run: 1 = chunked stretches (eviction-free), 0 = per-round
     uint32_t* nuns;           // per trace: unservable requests (0 -> identity pending list)
     int* bulkP;               // per trace: bulk prefix length (0: no bulk admission)
     long long* eoff;          // per trace + 1: exclusive scan of bulkP
@@ -51,6 +53,7 @@ size_t work_zero_bytes(int32_t n_traces);  // leading bytes of the workspace zer
 // grid-wide prepass: request init, per-trace tallies, bulk-admission sort
 int launch_prepass(const KArgs& a, void* stream);
 int launch_sched(const KArgs& a, int blocks, void* stream);
+int sched_launches(int policy);  // scheduler kernel launches per run
 int sched_smem_bytes();
 int sched_max_blocks(int policy, int* sm_count);
 

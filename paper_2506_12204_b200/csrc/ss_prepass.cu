@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(PP_THREADS) init_kernel(const __grid_constant_
         const long long g = base + threadIdx.x;
         const bool v = g < n;
         int t = -1;
-        unsigned long long tok = 0;
+        unsigned long long tok = 0, foot = 0;
         uint32_t uns = 0;
         if (v) {
             t = upper_index(A.in.trace_offsets, T, g);
@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(PP_THREADS) init_kernel(const __grid_constant_
             A.out.req.finish_time[g] = __longlong_as_double(0x7ff8000000000000ll);
             A.out.req.evictions[g] = 0u;
             tok = tout;
+            foot = (unsigned long long)prompt + (tout > mid ? tout : mid) + 1u;
             uns = serv ? 0u : 1u;
         }
         // warp-aggregated per-trace tallies (traces are contiguous in g, so a
@@ -169,10 +170,37 @@ __global__ void __launch_bounds__(PP_THREADS) init_kernel(const __grid_constant_
         const uint32_t s_lo = __reduce_add_sync(peers, (uint32_t)(tok & 0xffffu));
         const uint32_t s_hi = __reduce_add_sync(peers, (uint32_t)(tok >> 16));
         const uint32_t s_un = __reduce_add_sync(peers, uns);
+        const uint32_t f_lo = __reduce_add_sync(peers, (uint32_t)(foot & 0xffffu));
+        const uint32_t f_hi = __reduce_add_sync(peers, (uint32_t)(foot >> 16));
         if (v && lane == __ffs(peers) - 1) {
             atomicAdd(&A.w.tok[t], (unsigned long long)s_lo + ((unsigned long long)s_hi << 16));
+            atomicAdd(&A.w.foot[t], (unsigned long long)f_lo + ((unsigned long long)f_hi << 16));
             if (s_un) atomicAdd(&A.w.nuns[t], s_un);
         }
+    }
+}
+
+// ---- 2b. scheduler variant: chunked stretches only where the KV budget can never
+// bind (twice the largest per-trace footprint bound fits), i.e. no trace can
+// ever evict; tight budgets keep the per-round variant (shorter stretches).
+__global__ void __launch_bounds__(1024) select_kernel(const __grid_constant__ KArgs A) {
+    __shared__ unsigned long long wmax[32];
+    const int T = A.in.n_traces;
+    unsigned long long mx = 0;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) mx = A.w.foot[t] > mx ? A.w.foot[t] : mx;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(FULL, mx, o);
+        mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); i++) mx = wmax[i] > mx ? wmax[i] : mx;
+        const long long cap = A.P.memory_capacity;
+        int sel = (cap > 0 && mx <= (unsigned long long)cap / 2) ? 1 : 0;
+        if (A.P.flags & SS_FLAG_FORCE_CHUNKED) sel = 1;
+        if (A.P.flags & SS_FLAG_FORCE_PERROUND) sel = 0;
+        *A.w.sel = sel;
     }
 }
 
@@ -415,6 +443,7 @@ int launch_prepass(const KArgs& a, void* stream) {
         long long need = (n + PP_THREADS - 1) / PP_THREADS;
         init_kernel<<<(int)(need < grid ? need : grid), PP_THREADS, 0, st>>>(a);
     }
+    select_kernel<<<1, 1024, 0, st>>>(a);
     if (a.P.bulk_min < 0 || n == 0) return cudaGetLastError() == cudaSuccess ? SS_OK : SS_ERR_CUDA;
     keys_kernel<<<grid, PP_THREADS, 0, st>>>(a);
     hist_kernel<<<sms * 2, PP_THREADS, 0, st>>>(a);

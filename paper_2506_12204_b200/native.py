@@ -72,7 +72,10 @@ def launches_per_run(params=None, max_trace_len=None) -> int:
     bulk = params is None or params.bulk_min >= 0
     if params is not None and max_trace_len is not None:
         bulk = _bulk_possible(params, max_trace_len)
-    return 3 + (3 + 16 * 3 + 1 if bulk else 0) + 1
+    # detect, scan, init, select (+ the bulk sort) + the scheduler: semantic runs
+    # launch the chunked and the per-round variant, the unselected one exits at once
+    sched = 2 if params is None or params.policy == A.SS_POLICY["semantic"] else 1
+    return 4 + (3 + 16 * 3 + 1 if bulk else 0) + sched
 
 
 def _bulk_possible(params, max_trace_len: int) -> bool:

@@ -16,6 +16,9 @@ pytestmark = pytest.mark.gpu
 SMALL = golden_cases("small")
 LARGE = golden_cases("large")
 ANOM = golden_cases("anomaly")
+# both scheduler variants (chunked stretches / one round per step) on every case
+VARIANTS = {"chunked": A.SS_FLAG_FORCE_CHUNKED, "perround": A.SS_FLAG_FORCE_PERROUND}
+variants = pytest.mark.parametrize("variant", list(VARIANTS))
 
 
 @pytest.fixture(scope="module")
@@ -27,23 +30,26 @@ def native():
 
 
 @pytest.mark.parametrize("case", SMALL, ids=[c["name"] for c in SMALL])
-def test_gpu_matches_reference_small(native, case):
+@variants
+def test_gpu_matches_reference_small(native, case, variant):
     batch = case_batch(case)
-    res = native.run_host(case_params(case, A.SS_FLAG_DIGEST), batch, want_log=True)
+    res = native.run_host(case_params(case, A.SS_FLAG_DIGEST | VARIANTS[variant]), batch, want_log=True)
     check_against_golden(res, case, batch=batch)
 
 
 @pytest.mark.parametrize("case", LARGE, ids=[c["name"] for c in LARGE])
-def test_gpu_matches_reference_large(native, case):
+@variants
+def test_gpu_matches_reference_large(native, case, variant):
     batch = case_batch(case)
-    res = native.run_host(case_params(case, A.SS_FLAG_DIGEST), batch, want_log=False)
+    res = native.run_host(case_params(case, A.SS_FLAG_DIGEST | VARIANTS[variant]), batch, want_log=False)
     check_against_golden(res, case, batch=batch)
 
 
 @pytest.mark.parametrize("case", ANOM, ids=[c["name"] for c in ANOM])
-def test_gpu_matches_reference_stale_entries(native, case):
+@variants
+def test_gpu_matches_reference_stale_entries(native, case, variant):
     batch = case_batch(case)
-    res = native.run_host(case_params(case, A.SS_FLAG_DIGEST), batch, want_log=True)
+    res = native.run_host(case_params(case, A.SS_FLAG_DIGEST | VARIANTS[variant]), batch, want_log=True)
     if "ref_error" in case["expected"]:
         assert int(res.stats["status"][0]) == A.SS_TRACE_REF_ERROR
         assert int(res.stats["rounds"][0]) == case["expected"]["rounds_before_error"] + 1
@@ -93,18 +99,20 @@ def _compare_with_oracle(gpu, cpu, batch):
 
 
 @pytest.mark.parametrize("capacity", [10**9, 1500, 700])
-def test_gpu_many_traces_vs_oracle(native, capacity):
+@variants
+def test_gpu_many_traces_vs_oracle(native, capacity, variant):
     from oracle_binding import run_oracle
     from paper_2506_12204_b200.results import make_params
 
     batch, cfg = _seeded_batch(96, 300, dict(levels=3))
-    p = lambda: make_params(cfg.gpu_profile(), 16, capacity, levels=3, flags=A.SS_FLAG_DIGEST)
-    gpu = native.run_host(p(), batch)
+    p = lambda f=0: make_params(cfg.gpu_profile(), 16, capacity, levels=3, flags=A.SS_FLAG_DIGEST | f)
+    gpu = native.run_host(p(VARIANTS[variant]), batch)
     cpu = run_oracle(p(), batch, threads=8)
     assert _compare_with_oracle(gpu, cpu, batch) >= batch.n_traces // 2
 
 
-def test_gpu_config_d_sample_vs_oracle(native):
+@variants
+def test_gpu_config_d_sample_vs_oracle(native, variant):
     """Config D at bench shape (1,000 requests, 3 levels, 2,295 slots): heavy
     eviction, lost decisions, stale heap entries and reference exceptions.
     Status and rounds must agree on every trace, everything else where the
@@ -117,8 +125,8 @@ def test_gpu_config_d_sample_vs_oracle(native):
     from paper_2506_12204_b200.workload import WorkloadSpec
 
     batch = generate_batch(WorkloadSpec(total_requests=1000, levels=3), shard_seeds(64, 0), pinned=False)
-    p = lambda: make_params(get_profile("a100_qwen7b"), 16, 2295, levels=3, flags=A.SS_FLAG_DIGEST)
-    gpu = native.run_host(p(), batch)
+    p = lambda f=0: make_params(get_profile("a100_qwen7b"), 16, 2295, levels=3, flags=A.SS_FLAG_DIGEST | f)
+    gpu = native.run_host(p(VARIANTS[variant]), batch)
     cpu = run_oracle(p(), batch, threads=8)
     assert (cpu.stats["status"] == A.SS_TRACE_REF_ERROR).any()  # the sample covers an exception
     _compare_with_oracle(gpu, cpu, batch)
