@@ -577,7 +577,7 @@ __device__ __noinline__ bool queue_has_stale(const KArgs* Ap, const WarpSmem* sm
 
 // ---- SS_DEBUG_TIMING builds: warp-cycles per kernel section -----------------
 #ifdef SS_DEBUG_TIMING
-__device__ unsigned long long g_dbg_cycles[16];
+__device__ unsigned long long g_dbg_cycles[24];
 #define SS_SECT(s_)                                                   \
     do {                                                              \
         const long long now_ = clock64();                             \
@@ -585,13 +585,14 @@ __device__ unsigned long long g_dbg_cycles[16];
         dbg_t = now_;                                                 \
         dbg_cur = (s_);                                               \
     } while (0)
-#define SS_DCOUNT(k_, v_) (dbg_acc[8 + (k_)] += (unsigned long long)(v_))
+#define SS_DCOUNT(k_, v_) (dbg_acc[16 + (k_)] += (unsigned long long)(v_))
 #else
 #define SS_SECT(s_) ((void)0)
 #define SS_DCOUNT(k_, v_) ((void)0)
 #endif
 // sections: 0 init/admission/top, 1 fast path per-round body, 2 chunk, 3 general round, 4 outputs,
-// 5 stretch entry, 6 stretch round vote, 7 stretch order check
+// 5 stretch entry, 6 stretch round vote, 7 stretch order check; general round: 3 composition,
+// 8 KV admission, 9 batch duration, 10 progress, 11 record, 12 ongoing rebuild, 13 queue rebuild
 // counters: 8 chunks, 9 chunk rounds, 10 per-round fast rounds, 11 general rounds
 
 // ---- per-lane member quantities (32-bit: token counts of one request) -------
@@ -637,7 +638,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
     constexpr bool chunking = (MODE & 4) != 0;
     if (POL == SS_POLICY_SEMANTIC && *A.w.sel != (chunking ? 1 : 0)) return;
 #ifdef SS_DEBUG_TIMING
-    unsigned long long dbg_acc[16] = {0};
+    unsigned long long dbg_acc[24] = {0};
     long long dbg_t = clock64();
     int dbg_cur = 0;
 #endif
@@ -1336,6 +1337,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             }
 
             // ---- admission with KV budget (engine.py:296-327)
+            SS_SECT(8);
             MemQ q = mem_q(mem);
             {
                 int excl;
@@ -1496,6 +1498,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 if (R.ndec == 0 && c.nuns == nuns_start && nO_start == 0) set_status(T, SS_TRACE_LIVELOCK);
             } else {
                 // ---- batch_duration (engine.py:126-149) over granted copies
+                SS_SECT(9);
                 q = mem_q(mem);
                 double total = 0.0;
                 const unsigned pre = __ballot_sync(FULL, g_act && !q.isdec);
@@ -1536,6 +1539,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 const double end = ss::add(T.clock, total);
 
                 // ---- per-member progress (engine.py:351-363, 382-421)
+                SS_SECT(10);
                 bool done = false;
                 bool dups = false;
                 if (uni(anom)) {
@@ -1686,6 +1690,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     }
                 }
                 // ---- ITERATION_END record (engine.py:365-380) + digest
+                SS_SECT(11);
                 const unsigned cdone = __ballot_sync(FULL, done);
                 const int nc_done = __popc(cdone);
                 const int gi = __popc(R.G & lt), ci = __popc(cdone & lt);
@@ -1730,6 +1735,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 T.clock = end;
                 T.rounds += 1;
                 // ---- ongoing = granted copies not completed, in granted order
+                SS_SECT(12);
                 const bool stay = g_act && (mem.flg & F_STAGE) != ST_DONE;
                 const unsigned smk = __ballot_sync(FULL, stay);
                 __syncwarp();
@@ -1771,6 +1777,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             if (T.rounds >= round_cap) set_status(T, SS_TRACE_ROUND_CAP);
 
             // ---- queue rebuild: drop popped FRONT entries, then insert this
+            SS_SECT(13);
             //      round's pushed-back / failed / evicted requests with the key
             //      they were queued with (the heap stores keys at insert time)
             f_compact(E, T, R.rmF);
@@ -1870,7 +1877,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
 #ifdef SS_DEBUG_TIMING
     SS_SECT(0);
     if (lane == 0)
-        for (int i = 0; i < 16; i++) atomicAdd(&g_dbg_cycles[i], dbg_acc[i]);
+        for (int i = 0; i < 24; i++) atomicAdd(&g_dbg_cycles[i], dbg_acc[i]);
 #endif
 }
 
@@ -1986,8 +1993,8 @@ int sched_launches(int policy) { return policy == SS_POLICY_SEMANTIC ? 2 : 1; }
 // debug builds only (not part of include/semsched_b200.h): read and clear the section counters
 extern "C" int ss_debug_cycles(unsigned long long* out) {
     cudaDeviceSynchronize();
-    if (cudaMemcpyFromSymbol(out, ss::g_dbg_cycles, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
-    unsigned long long z[16] = {0};
+    if (cudaMemcpyFromSymbol(out, ss::g_dbg_cycles, sizeof(unsigned long long) * 24) != cudaSuccess) return -1;
+    unsigned long long z[24] = {0};
     return cudaMemcpyToSymbol(ss::g_dbg_cycles, z, sizeof(z)) == cudaSuccess ? 0 : -1;
 }
 #endif

@@ -14,19 +14,21 @@ T = int(sys.argv[2]) if len(sys.argv) > 2 else wl["traces"]
 batch, T = bench.build_batch(wl, 0, T, pinned=False)
 prm = make_params(get_profile(wl["profile"]), 16, wl["capacity"], levels=wl["levels"], flags=A.SS_FLAG_DIGEST)
 lib = native.lib()
-buf = (C.c_ulonglong * 16)()
+buf = (C.c_ulonglong * 24)()
 native.run_host(prm, batch)  # warm-up
 lib.ss_debug_cycles(buf)
 res = native.run_host(prm, batch)
 lib.ss_debug_cycles(buf)
 v = list(buf)
-tot = sum(v[:8]) or 1
-names = ["init/admission/top", "fast per-round body", "chunk", "general round", "outputs", "stretch entry", "stretch vote", "stretch order"]
+tot = sum(v[:16]) or 1
+names = ["init/admission/top", "fast per-round body", "chunk", "g: composition", "outputs", "stretch entry", "stretch vote", "stretch order",
+         "g: KV admission", "g: batch duration", "g: progress", "g: record", "g: ongoing rebuild", "g: queue rebuild"]
 rounds = int(res.stats["rounds"].sum())
 print(f"{W}: {T} traces, {rounds} rounds, kernel {res.kernel_ms:.2f} ms")
 for i, n in enumerate(names):
     print(f"  {n:20s} {100 * v[i] / tot:5.1f}%  {v[i] / max(rounds, 1):8.1f} warp-cycles/round")
-print(f"  chunks {v[8]}, chunk rounds {v[9]} ({v[9] / max(v[8], 1):.1f}/chunk), per-round fast {v[10]}, general {v[11]}")
-if v[8]: print(f"  cycles/chunk {v[2] / v[8]:.0f}, per chunk round {v[2] / max(v[9], 1):.0f}")
-if v[10]: print(f"  cycles per per-round fast round {v[1] / v[10]:.0f} (incl. stretch setup/exit)")
-if v[11]: print(f"  cycles per general round {v[3] / v[11]:.0f}")
+c = v[16:]
+print(f"  chunks {c[0]}, chunk rounds {c[1]} ({c[1] / max(c[0], 1):.1f}/chunk), per-round fast {c[2]}, general {c[3]}")
+if c[0]: print(f"  cycles/chunk {v[2] / c[0]:.0f}, per chunk round {v[2] / max(c[1], 1):.0f}")
+if c[2]: print(f"  cycles per per-round fast round {v[1] / c[2]:.0f}")
+if c[3]: print(f"  cycles per general round (composition .. queue rebuild) {sum(v[i] for i in (3, 8, 9, 10, 11, 12, 13)) / c[3]:.0f}")
