@@ -1264,7 +1264,12 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             if (c_sel) {
                 MemS cm;
                 load_mem(A, T.off, ck.aux & SLOT_MASK, cm);
-                cm.flg = flg_update(A, T.off + cm.slot, F_Q, 0u);  // popped from the heap for good
+                if (anom) {  // another copy may have moved the flags: re-read them
+                    cm.flg = flg_update(A, T.off + cm.slot, F_Q, 0u);  // popped from the heap for good
+                } else {  // distinct requests: the loaded flags are current
+                    cm.flg &= ~F_Q;
+                    *FLG(A, T.off + cm.slot) = cm.flg;
+                }
                 sm->M[cnt_c] = cm;
             }
             if (!direct && has_o && cnt_o < m) sm->M[cnt_o] = sm->OM[lane];
