@@ -728,35 +728,35 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     T.nRun = c.bulk;
                 }
                 const bool dn = c.dense != 0;
+                // ready times and admission keys (prepass, k0) of the next 32 pending
+                // requests load together; the first one not admitted is the next ready time
+                double nr = INFINITY;
                 while (uni(T.cursor < T.npend)) {
                     int i = T.cursor + lane;
                     bool v = i < T.npend;
                     uint32_t s = 0;
-                    bool ok = false;
+                    double rdy = INFINITY;
+                    Key k;
                     if (v) {
                         s = dn ? (uint32_t)i : A.w.pend[T.off + i];
-                        ok = A.in.ready_time[T.off + s] <= thr;
+                        rdy = A.in.ready_time[T.off + s];
+                        k = reinterpret_cast<const Key*>(A.w.k0)[T.off + s];
                     }
+                    const bool ok = rdy <= thr;
                     unsigned am = __ballot_sync(FULL, ok);
                     int cnt = am == FULL ? 32 : __ffs(~am) - 1;
+                    nr = __shfl_sync(FULL, rdy, cnt & 31);
                     if (cnt == 0) break;
                     bool mine = lane < cnt;
-                    Key k;
-                    if (mine) {
-                        long long g = T.off + s;
-                        *FLG(A, g) = ST_WAIT | F_Q;
-                        const uint32_t w = STA(A)[g].w;
-                        k = make_key<POL>(w >> 24, DYN(A)[g].ft, w & SLOT_MASK, s, false);
-                    }
+                    if (mine) *FLG(A, T.off + s) = ST_WAIT | F_Q;
                     const int2 qs = q_insert32(&A, sm, T.off, T.nF, T.nB, T.nRun, k, mine);
                     T.nF = qs.x;
                     T.nB = qs.y;
                     T.cursor += cnt;
                     if (cnt < 32) break;
+                    nr = INFINITY;
                 }
-                T.next_ready = T.cursor < T.npend
-                                   ? A.in.ready_time[T.off + (dn ? T.cursor : A.w.pend[T.off + T.cursor])]
-                                   : INFINITY;
+                T.next_ready = nr;
             }
             const int live = T.nF + T.nB + T.nO + T.nRun;
             if (uni(live == 0)) {
@@ -1897,8 +1897,8 @@ static long long tiles_for(int64_t n) { return ((n > 0 ? n : 1) + RS_TILE - 1) /
 size_t work_bytes(int64_t n, int32_t T) {
     size_t nn = (size_t)(n > 0 ? n : 1), tt = (size_t)(T > 0 ? T : 1);
     size_t zero = 2 * align16(tt * 8) + align16(tt * 4) + align16((size_t)RS_PASSES * 256 * 4) + 16;
-    // st, dy, B, ins, S: 16 B; rpos, R, pend, tt0, tt1: 4 B
-    return zero + 5 * align16(nn * 16) + 5 * align16(nn * 4) + align16(tt * 4) + align16((tt + 1) * 8) +
+    // st, dy, B, ins, S, k0: 16 B; rpos, R, pend, tt0, tt1: 4 B
+    return zero + 6 * align16(nn * 16) + 5 * align16(nn * 4) + align16(tt * 4) + align16((tt + 1) * 8) +
            align16((size_t)(RS_PASSES + 1) * 4) + align16((size_t)256 * tiles_for(n) * 4);
 }
 
@@ -1920,6 +1920,7 @@ void carve_work(void* base, int64_t n, int32_t T, Work* w) {
     w->B = (void*)p;         p += align16(nn * 16);
     w->ins = (void*)p;       p += align16(nn * 16);
     w->S = (void*)p;         p += align16(nn * 16);
+    w->k0 = (void*)p;        p += align16(nn * 16);
     w->rpos = (uint32_t*)p;  p += align16(nn * 4);
     w->R = (uint32_t*)p;     p += align16(nn * 4);
     w->pend = (uint32_t*)p;  p += align16(nn * 4);

@@ -18,6 +18,7 @@ struct Work {
     uint32_t* R;         // resident list (eviction candidates)
     uint32_t* pend;      // servable requests in pending order
     void* ins;           // this round's re-queue list: 16-byte keys (prepass: sort ping-pong)
+    void* k0;            // dispatch key of each request at admission (prepass; read by the admission loop)
     // ---- prepass (ss_prepass.cu) -------------------------------------------
     void* S;                  // sorted bulk runs: 16-byte keys, trace t at [eoff[t], eoff[t] + bulkP[t])
     uint32_t* tt0;            // radix sort payload: trace index of each key (ping-pong pair)

@@ -157,6 +157,16 @@ __global__ void __launch_bounds__(PP_THREADS) init_kernel(const __grid_constant_
             d.dec = 0u;
             d.flg = flg;
             DYN[g] = d;
+            // dispatch key at admission (engine.py:204-206 -> heaps.py insert)
+            const uint32_t rk = A.in.pred_urgency[g], tie = A.in.tie_rank[g], sl = (uint32_t)i;
+            Key k;
+            switch (A.P.policy) {
+            case SS_POLICY_FCFS: k = make_key<SS_POLICY_FCFS>(rk, d.ft, tie, sl, false); break;
+            case SS_POLICY_SJF: k = make_key<SS_POLICY_SJF>(rk, d.ft, tie, sl, false); break;
+            case SS_POLICY_HPJF: k = make_key<SS_POLICY_HPJF>(rk, d.ft, tie, sl, false); break;
+            default: k = make_key<SS_POLICY_SEMANTIC>(rk, d.ft, tie, sl, false); break;
+            }
+            reinterpret_cast<Key*>(A.w.k0)[g] = k;
             A.out.req.first_scheduled[g] = __longlong_as_double(0x7ff8000000000000ll);
             A.out.req.finish_time[g] = __longlong_as_double(0x7ff8000000000000ll);
             A.out.req.evictions[g] = 0u;
