@@ -57,9 +57,13 @@ int validate(const ss_params* p, const ss_trace_batch* b, const ss_outputs* o) {
 
 struct HostStage {
     std::mutex mu;
-    void* buf = nullptr;
+    void* buf = nullptr;   // device: inputs | outputs | log | offsets | workspaces
     size_t cap = 0;
+    void* hbuf = nullptr;  // pinned host: the slices' rebased offsets
+    size_t hcap = 0;
+    cudaStream_t streams[4] = {nullptr, nullptr, nullptr, nullptr};
 };
+constexpr int32_t SLICE_TRACES = 1024;  // ss_run_traces_host pipelines batches of >= 2 slices
 HostStage g_stage;
 
 size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -184,30 +188,29 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
         if (kernel_ms) *kernel_ms = 0.f;
         return SS_OK;
     }
-    const size_t nn = (size_t)(n > 0 ? n : 1);
     const bool logr = (params->flags & SS_FLAG_ROUND_LOG) != 0;
-    int64_t log_words = 0;
-    if (logr) log_words = ho->log_offsets[T];
-    // one device allocation: inputs | outputs | log | workspace
-    size_t in_b = a16((T + 1) * 8) + 2 * a16(nn * 8) + 3 * a16(nn * 4) + 2 * a16(nn) + a16(nn * 4);
-    size_t out_b = 2 * a16(nn * 8) + 2 * a16(nn * 4) + a16(nn * 8) + a16(nn * 4) +
-                   a16((size_t)T * sizeof(ss_trace_stats)) + a16(nn * 4);
-    size_t log_b = logr ? a16((size_t)log_words * 4) + a16((T + 1) * 8) : 0;
-    size_t ws_b = ss::work_bytes(n, T);
-    // no trace long enough for a bulk first round: skip the bulk-sort stage
-    ss_params pp = *params;
-    if (pp.bulk_min == 0) {
-        int64_t maxlen = 0;
-        for (int32_t t = 0; t < T; t++) {
-            const int64_t k = hb->trace_offsets[t + 1] - hb->trace_offsets[t];
-            if (k > maxlen) maxlen = k;
-        }
-        if (maxlen < SS_BULK_MIN_DEFAULT) pp.bulk_min = -1;
+    // Slices of consecutive traces, each on its own stream: slice s+1's inputs
+    // upload while slice s computes, slice s's outputs download while later
+    // slices compute, and a later slice's CTAs fill the SM slots an earlier
+    // slice's finished warps free. Every slice is an independent ss_run_traces.
+    const int S = T >= 4 * SLICE_TRACES ? 4 : (T >= 2 * SLICE_TRACES ? 2 : 1);
+    int32_t t0s[5];
+    for (int s = 0; s <= S; s++) t0s[s] = (int32_t)((int64_t)T * s / S);
+    size_t in_b = 2 * a16((size_t)(n > 0 ? n : 1) * 8) + 4 * a16((size_t)(n > 0 ? n : 1) * 4) +
+                  2 * a16((size_t)(n > 0 ? n : 1));
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    size_t out_b = 3 * a16(nn * 8) + 3 * a16(nn * 4) + a16((size_t)T * sizeof(ss_trace_stats)) + a16(nn * 4);
+    const int64_t log_words = logr ? ho->log_offsets[T] : 0;
+    size_t log_b = logr ? a16((size_t)log_words * 4) : 0;
+    size_t off_b = 0, ws_b = 0;
+    for (int s = 0; s < S; s++) {
+        const int32_t Ts = t0s[s + 1] - t0s[s];
+        const int64_t ns = hb->trace_offsets[t0s[s + 1]] - hb->trace_offsets[t0s[s]];
+        off_b += a16((size_t)(Ts + 1) * 8) * (logr ? 2 : 1);
+        ws_b += a16(ss::work_bytes(ns, Ts));
     }
-    params = &pp;
-    size_t total = in_b + out_b + log_b + ws_b;
+    const size_t total = a16(in_b) + a16(out_b) + a16(log_b) + a16(off_b) + a16(ws_b);
     std::lock_guard<std::mutex> lk(g_stage.mu);
-    cudaStream_t st = (cudaStream_t)stream;
     if (g_stage.cap < total) {
         if (g_stage.buf) CK(cudaFree(g_stage.buf));
         g_stage.buf = nullptr;
@@ -215,33 +218,33 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
         CK(cudaMalloc(&g_stage.buf, total));
         g_stage.cap = total;
     }
+    if (g_stage.hcap < off_b) {  // pinned staging of the slices' rebased offsets
+        if (g_stage.hbuf) CK(cudaFreeHost(g_stage.hbuf));
+        g_stage.hbuf = nullptr;
+        g_stage.hcap = 0;
+        CK(cudaMallocHost(&g_stage.hbuf, off_b));
+        g_stage.hcap = off_b;
+    }
+    for (int s = 0; s < S; s++)
+        if (!g_stage.streams[s]) CK(cudaStreamCreateWithFlags(&g_stage.streams[s], cudaStreamNonBlocking));
     char* p = (char*)g_stage.buf;
     auto take = [&](size_t bytes) {
         char* r = p;
         p += a16(bytes);
         return (void*)r;
     };
+    // whole-batch device arrays; slice s works on its request / trace range
     ss_trace_batch db = *hb;
+    db.ready_time = (double*)take(nn * 8);
+    db.arrival_time = (double*)take(nn * 8);
+    db.prompt_len = (uint32_t*)take(nn * 4);
+    db.true_output_len = (uint32_t*)take(nn * 4);
+    db.pred_len = (uint32_t*)take(nn * 4);
+    db.pred_urgency = (uint8_t*)take(nn);
+    db.true_urgency = (uint8_t*)take(nn);
+    db.tie_rank = (uint32_t*)take(nn * 4);
     ss_outputs dout;
     memset(&dout, 0, sizeof dout);
-    int64_t* d_off = (int64_t*)take((T + 1) * 8);
-    CK(cudaMemcpyAsync(d_off, hb->trace_offsets, (T + 1) * 8, cudaMemcpyHostToDevice, st));
-    db.trace_offsets = d_off;
-#define H2D(field, bytes)                                                               \
-    do {                                                                                \
-        void* d_ = take(bytes);                                                         \
-        if (n > 0) CK(cudaMemcpyAsync(d_, hb->field, bytes, cudaMemcpyHostToDevice, st)); \
-        db.field = (decltype(db.field))d_;                                              \
-    } while (0)
-    H2D(ready_time, nn * 8);
-    H2D(arrival_time, nn * 8);
-    H2D(prompt_len, nn * 4);
-    H2D(true_output_len, nn * 4);
-    H2D(pred_len, nn * 4);
-    H2D(pred_urgency, nn);
-    H2D(true_urgency, nn);
-    H2D(tie_rank, nn * 4);
-#undef H2D
     dout.req.first_scheduled = (double*)take(nn * 8);
     dout.req.finish_time = (double*)take(nn * 8);
     dout.req.generated = (uint32_t*)take(nn * 4);
@@ -252,29 +255,116 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
     dout.req.state = ho->req.state ? (uint32_t*)d_state : nullptr;
     dout.stats = (ss_trace_stats*)take((size_t)T * sizeof(ss_trace_stats));
     dout.unservable_slots = (uint32_t*)take(nn * 4);
-    if (logr) {
-        dout.round_log = (uint32_t*)take((size_t)log_words * 4);
-        int64_t* d_loff = (int64_t*)take((T + 1) * 8);
-        CK(cudaMemcpyAsync(d_loff, ho->log_offsets, (T + 1) * 8, cudaMemcpyHostToDevice, st));
-        dout.log_offsets = d_loff;
+    if (logr) dout.round_log = (uint32_t*)take((size_t)log_words * 4);
+    char* d_offs = (char*)take(off_b);
+    char* d_ws = (char*)take(ws_b);
+    char* h_offs = (char*)g_stage.hbuf;
+    // the slices start after the caller's stream work
+    cudaStream_t cs = (cudaStream_t)stream;
+    cudaEvent_t ev_in = nullptr, ev_k0 = nullptr, ev_k1[4] = {nullptr, nullptr, nullptr, nullptr};
+    CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev_in, cs));
+    if (kernel_ms && S > 1) {
+        CK(cudaEventCreate(&ev_k0));
+        for (int s = 0; s < S; s++) CK(cudaEventCreate(&ev_k1[s]));
     }
-    void* ws = take(ws_b);
-    rc = ss_run_traces(params, &db, &dout, ws, ws_b, stream, kernel_ms);
-    if (rc) return rc;
+    size_t ooff = 0, wsoff = 0;
+    for (int s = 0; s < S; s++) {
+        cudaStream_t st = g_stage.streams[s];
+        CK(cudaStreamWaitEvent(st, ev_in, 0));
+        const int32_t ta = t0s[s], Ts = t0s[s + 1] - t0s[s];
+        const int64_t ra = hb->trace_offsets[ta], ns = hb->trace_offsets[t0s[s + 1]] - ra;
+        // rebased trace (and log) offsets of this slice
+        int64_t* ho_off = (int64_t*)(h_offs + ooff);
+        int64_t* do_off = (int64_t*)(d_offs + ooff);
+        for (int32_t t = 0; t <= Ts; t++) ho_off[t] = hb->trace_offsets[ta + t] - ra;
+        CK(cudaMemcpyAsync(do_off, ho_off, (size_t)(Ts + 1) * 8, cudaMemcpyHostToDevice, st));
+        ooff += a16((size_t)(Ts + 1) * 8);
+        ss_trace_batch sb = db;
+        sb.n_traces = Ts;
+        sb.n_requests = ns;
+        sb.trace_offsets = do_off;
+#define H2D(field, esz)                                                                                  \
+    do {                                                                                                 \
+        sb.field = db.field + ra;                                                                        \
+        if (ns > 0) CK(cudaMemcpyAsync((void*)sb.field, hb->field + ra, (size_t)ns * (esz), cudaMemcpyHostToDevice, st)); \
+    } while (0)
+        H2D(ready_time, 8);
+        H2D(arrival_time, 8);
+        H2D(prompt_len, 4);
+        H2D(true_output_len, 4);
+        H2D(pred_len, 4);
+        H2D(pred_urgency, 1);
+        H2D(true_urgency, 1);
+        H2D(tie_rank, 4);
+#undef H2D
+        ss_outputs so = dout;
+        so.req.first_scheduled += ra;
+        so.req.finish_time += ra;
+        so.req.generated += ra;
+        so.req.evictions += ra;
+        if (so.req.f_t) so.req.f_t += ra;
+        if (so.req.state) so.req.state += ra;
+        so.stats += ta;
+        so.unservable_slots += ra;
+        int64_t la = 0, lw = 0;
+        if (logr) {
+            la = ho->log_offsets[ta];
+            lw = ho->log_offsets[t0s[s + 1]] - la;
+            int64_t* hl = (int64_t*)(h_offs + ooff);
+            int64_t* dl = (int64_t*)(d_offs + ooff);
+            for (int32_t t = 0; t <= Ts; t++) hl[t] = ho->log_offsets[ta + t] - la;
+            CK(cudaMemcpyAsync(dl, hl, (size_t)(Ts + 1) * 8, cudaMemcpyHostToDevice, st));
+            ooff += a16((size_t)(Ts + 1) * 8);
+            so.round_log += la;
+            so.log_offsets = dl;
+        }
+        // no trace of the slice long enough for a bulk first round: skip the bulk-sort stage
+        ss_params pp = *params;
+        if (pp.bulk_min == 0) {
+            int64_t maxlen = 0;
+            for (int32_t t = ta; t < ta + Ts; t++) {
+                const int64_t k = hb->trace_offsets[t + 1] - hb->trace_offsets[t];
+                if (k > maxlen) maxlen = k;
+            }
+            if (maxlen < SS_BULK_MIN_DEFAULT) pp.bulk_min = -1;
+        }
+        const size_t wsz = ss::work_bytes(ns, Ts);
+        if (ev_k0 && s == 0) CK(cudaEventRecord(ev_k0, st));
+        // one slice: the call times its prepass and kernel itself (ss_last_timings)
+        rc = ss_run_traces(&pp, &sb, &so, d_ws + wsoff, wsz, (void*)st, S == 1 ? kernel_ms : nullptr);
+        if (rc) return rc;
+        wsoff += a16(wsz);
+        if (ev_k0) CK(cudaEventRecord(ev_k1[s], st));
 #define D2H(dst, src, bytes) \
     if ((dst) && (bytes) > 0) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st))
-    size_t nb = (size_t)n;
-    D2H(ho->req.first_scheduled, dout.req.first_scheduled, nb * 8);
-    D2H(ho->req.finish_time, dout.req.finish_time, nb * 8);
-    D2H(ho->req.generated, dout.req.generated, nb * 4);
-    D2H(ho->req.evictions, dout.req.evictions, nb * 4);
-    D2H(ho->req.f_t, dout.req.f_t, nb * 8);
-    D2H(ho->req.state, dout.req.state, nb * 4);
-    D2H(ho->stats, dout.stats, (size_t)T * sizeof(ss_trace_stats));
-    D2H(ho->unservable_slots, dout.unservable_slots, nb * 4);
-    if (logr) D2H(ho->round_log, dout.round_log, (size_t)log_words * 4);
+        const size_t nb = (size_t)ns;
+        D2H(ho->req.first_scheduled + ra, so.req.first_scheduled, nb * 8);
+        D2H(ho->req.finish_time + ra, so.req.finish_time, nb * 8);
+        D2H(ho->req.generated + ra, so.req.generated, nb * 4);
+        D2H(ho->req.evictions + ra, so.req.evictions, nb * 4);
+        if (ho->req.f_t) D2H(ho->req.f_t + ra, so.req.f_t, nb * 8);
+        if (ho->req.state) D2H(ho->req.state + ra, so.req.state, nb * 4);
+        D2H(ho->stats + ta, so.stats, (size_t)Ts * sizeof(ss_trace_stats));
+        D2H(ho->unservable_slots + ra, so.unservable_slots, nb * 4);
+        if (logr) D2H(ho->round_log + la, so.round_log, (size_t)lw * 4);
 #undef D2H
-    CK(cudaStreamSynchronize(st));
+    }
+    for (int s = 0; s < S; s++) CK(cudaStreamSynchronize(g_stage.streams[s]));
+    cudaEventDestroy(ev_in);
+    if (kernel_ms && S > 1) {
+        // span from the first slice's prepass to the last kernel to finish
+        float mx = 0.f;
+        for (int s = 0; s < S; s++) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev_k0, ev_k1[s]));
+            mx = ms > mx ? ms : mx;
+            cudaEventDestroy(ev_k1[s]);
+        }
+        cudaEventDestroy(ev_k0);
+        *kernel_ms = g_kernel_ms = mx;
+        g_prepass_ms = 0.f;
+    }
     for (int32_t t = 0; t < T; t++)
         if (ho->stats[t].status != SS_TRACE_OK) return fail(SS_ERR_TRACE_FAILED, "a trace ended with a non-OK status");
     return SS_OK;

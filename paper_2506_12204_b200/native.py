@@ -176,7 +176,9 @@ def run_host(params, batch, want_log: bool = False, stream: int = 0, allow_trace
     rc = lib().ss_run_traces_host(C.byref(params), C.byref(hb), C.byref(o), C.c_void_p(stream), C.byref(ms))
     _check(rc, allow_trace_failed)
     res = collect(batch, outs, log, log_off, kernel_ms=ms.value)
-    if want_log and (res.stats["status"] == A.SS_TRACE_LOG_OVERFLOW).any():
+    # a trace whose log outgrew the first guess runs again with 4x the space; a trace the
+    # reference would never finish (livelock) overflows any log, so the retries are bounded
+    if want_log and (res.stats["status"] == A.SS_TRACE_LOG_OVERFLOW).any() and log_scale < 64:
         return run_host(params, batch, want_log, stream, allow_trace_failed, log_scale * 4)
     return res
 

@@ -381,3 +381,25 @@ def test_gpu_extreme_batch_sizes_tight_memory(native, b):
     for cap in (400, 2000):
         p = lambda: make_params(cfg.gpu_profile(), b, cap, levels=4, flags=A.SS_FLAG_DIGEST)
         _compare_with_oracle(native.run_host(p(), batch), run_oracle(p(), batch, threads=8), batch)
+
+
+@pytest.mark.parametrize("capacity", [10**9, 700])
+def test_gpu_pipelined_host_call_vs_oracle(native, capacity):
+    """ss_run_traces_host splits >= 2,048 traces into slices on separate streams
+    (uploads, kernels and downloads overlap); results, logs included, must equal
+    the oracle's on every trace, across uneven slice boundaries."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.results import make_params
+    from paper_2506_12204_b200.tracegen import generate_batch
+    from paper_2506_12204_b200.workload import WorkloadSpec
+
+    batch = generate_batch(WorkloadSpec(total_requests=40, levels=3), list(range(4099)), pinned=False)
+    logs = capacity > 10**6  # tight budgets can livelock a trace (no finite log)
+    p = lambda f=0: make_params(get_profile("a100_qwen7b"), 8, capacity, levels=3, flags=A.SS_FLAG_DIGEST | f)
+    gpu = native.run_host(p(), batch, want_log=logs)
+    cpu = run_oracle(p(A.SS_FLAG_ROUND_LOG if logs else 0), batch, threads=8)
+    assert _compare_with_oracle(gpu, cpu, batch) >= batch.n_traces // 2
+    if logs:
+        for t in range(0, batch.n_traces, 97):
+            assert np.array_equal(gpu.logs[t], cpu.logs[t]), t
