@@ -55,15 +55,21 @@ int validate(const ss_params* p, const ss_trace_batch* b, const ss_outputs* o) {
     return SS_OK;
 }
 
+#ifndef SS_SLICE_TRACES
+#define SS_SLICE_TRACES 1024  // ss_run_traces_host pipelines batches of >= 2 slices of this size
+#endif
+#ifndef SS_MAX_SLICES
+#define SS_MAX_SLICES 4
+#endif
 struct HostStage {
     std::mutex mu;
     void* buf = nullptr;   // device: inputs | outputs | log | offsets | workspaces
     size_t cap = 0;
     void* hbuf = nullptr;  // pinned host: the slices' rebased offsets
     size_t hcap = 0;
-    cudaStream_t streams[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t streams[SS_MAX_SLICES] = {};
 };
-constexpr int32_t SLICE_TRACES = 1024;  // ss_run_traces_host pipelines batches of >= 2 slices
+constexpr int32_t SLICE_TRACES = SS_SLICE_TRACES;
 HostStage g_stage;
 
 size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -193,8 +199,9 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
     // upload while slice s computes, slice s's outputs download while later
     // slices compute, and a later slice's CTAs fill the SM slots an earlier
     // slice's finished warps free. Every slice is an independent ss_run_traces.
-    const int S = T >= 4 * SLICE_TRACES ? 4 : (T >= 2 * SLICE_TRACES ? 2 : 1);
-    int32_t t0s[5];
+    int S = (int)(T / SLICE_TRACES);
+    S = S < 1 ? 1 : (S > SS_MAX_SLICES ? SS_MAX_SLICES : S);
+    int32_t t0s[SS_MAX_SLICES + 1];
     for (int s = 0; s <= S; s++) t0s[s] = (int32_t)((int64_t)T * s / S);
     size_t in_b = 2 * a16((size_t)(n > 0 ? n : 1) * 8) + 4 * a16((size_t)(n > 0 ? n : 1) * 4) +
                   2 * a16((size_t)(n > 0 ? n : 1));
@@ -261,7 +268,7 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
     char* h_offs = (char*)g_stage.hbuf;
     // the slices start after the caller's stream work
     cudaStream_t cs = (cudaStream_t)stream;
-    cudaEvent_t ev_in = nullptr, ev_k0 = nullptr, ev_k1[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_in = nullptr, ev_k0 = nullptr, ev_k1[SS_MAX_SLICES] = {};
     CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
     CK(cudaEventRecord(ev_in, cs));
     if (kernel_ms && S > 1) {
