@@ -434,6 +434,10 @@ SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot,
     const int lane = E.lane;
     Cold& c = E.sm->c;
     const ss_profile& P = A.P.profile;
+    if (uni(*A.w.sel == SS_SEL_NO_EVICT)) {  // the resident list is not kept in this regime
+        set_status(T, SS_TRACE_INTERNAL);
+        return false;
+    }
     Key best;
     bool have = false;
     int best_ri = -1;
@@ -636,7 +640,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
     // back to back; the one the prepass did not select (ss_prepass.cu
     // select_kernel: chunks only when the KV budget can never bind) exits at once.
     constexpr bool chunking = (MODE & 4) != 0;
-    if (POL == SS_POLICY_SEMANTIC && *A.w.sel != (chunking ? 1 : 0)) return;
+    const int sel = *A.w.sel;
+    if (POL == SS_POLICY_SEMANTIC && (sel != SS_SEL_PERROUND) != chunking) return;
+    // no trace can ever evict (select_kernel's footprint rule): the resident list
+    // (eviction candidates) is never read, so it is not maintained
+    const bool track_res = sel != SS_SEL_NO_EVICT;
 #ifdef SS_DEBUG_TIMING
     unsigned long long dbg_acc[24] = {0};
     long long dbg_t = clock64();
@@ -960,7 +968,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                 const int q = __ffs(cm) - 1;
                                 cm &= cm - 1;
                                 const uint32_t s = __shfl_sync(FULL, mem.slot, q);
-                                if (lane == 0) {
+                                if (track_res && lane == 0) {
                                     const uint32_t ri = A.w.rpos[T.off + s];
                                     const uint32_t last = A.w.R[T.off + T.nR - 1];
                                     A.w.R[T.off + ri] = last;
@@ -1586,7 +1594,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     if (T.used < 0) set_status(T, SS_TRACE_INTERNAL);
                     const unsigned nmr = __ballot_sync(FULL, newres);
                     if (nmr) {
-                        if (newres) {
+                        if (track_res && newres) {
                             const uint32_t idx = (uint32_t)(T.nR + __popc(nmr & lt));
                             A.w.R[T.off + idx] = mem.slot;
                             A.w.rpos[T.off + mem.slot] = idx;
@@ -1600,7 +1608,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             const int k = __ffs(cmk) - 1;
                             cmk &= cmk - 1;
                             const uint32_t s = __shfl_sync(FULL, mem.slot, k);
-                            if (lane == 0) {
+                            if (track_res && lane == 0) {
                                 const uint32_t ri = A.w.rpos[T.off + s];
                                 const uint32_t last = A.w.R[T.off + T.nR - 1];
                                 A.w.R[T.off + ri] = last;

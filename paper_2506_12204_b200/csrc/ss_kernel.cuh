@@ -6,6 +6,9 @@
 
 namespace ss {
 
+// select_kernel's choice: one round per step / chunked stretches with no eviction
+// possible (resident list not kept) / chunked stretches forced by the caller
+constexpr int SS_SEL_PERROUND = 0, SS_SEL_NO_EVICT = 1, SS_SEL_CHUNKED = 2;
 constexpr int FCAP = 64;  // sorted queue-front capacity per trace (shared memory)
 constexpr int WPB = 4;    // traces (warps) per CTA
 
@@ -25,7 +28,7 @@ struct Work {
     uint32_t* tt1;
     unsigned long long* tok;  // per trace: sum of true output lengths (round cap)
     unsigned long long* foot; // per trace: sum of prompt + max(true, predicted) output + 1 (KV footprint bound)
-    int* sel;                 // scheduler variant for this run: 1 = chunked stretches (eviction-free), 0 = per-round
+    int* sel;                 // scheduler variant for this run (SS_SEL_*)
     uint32_t* nuns;           // per trace: unservable requests (0 -> identity pending list)
     int* bulkP;               // per trace: bulk prefix length (0: no bulk admission)
     long long* eoff;          // per trace + 1: exclusive scan of bulkP

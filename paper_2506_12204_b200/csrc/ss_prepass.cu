@@ -207,9 +207,9 @@ __global__ void __launch_bounds__(1024) select_kernel(const __grid_constant__ KA
     if (threadIdx.x == 0) {
         for (int i = 1; i < (int)(blockDim.x >> 5); i++) mx = wmax[i] > mx ? wmax[i] : mx;
         const long long cap = A.P.memory_capacity;
-        int sel = (cap > 0 && mx <= (unsigned long long)cap / 2) ? 1 : 0;
-        if (A.P.flags & SS_FLAG_FORCE_CHUNKED) sel = 1;
-        if (A.P.flags & SS_FLAG_FORCE_PERROUND) sel = 0;
+        int sel = (cap > 0 && mx <= (unsigned long long)cap / 2) ? SS_SEL_NO_EVICT : SS_SEL_PERROUND;
+        if ((A.P.flags & SS_FLAG_FORCE_CHUNKED) && sel != SS_SEL_NO_EVICT) sel = SS_SEL_CHUNKED;
+        if (A.P.flags & SS_FLAG_FORCE_PERROUND) sel = SS_SEL_PERROUND;
         *A.w.sel = sel;
     }
 }
