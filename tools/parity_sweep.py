@@ -1,5 +1,5 @@
-"""Dev tool: GPU vs oracle digests over many traces of tight-memory configs.
-    python tools/parity_sweep.py <traces>"""
+"""Dev tool: GPU vs oracle digests over many traces of tight-memory and ample configs.
+    python tools/parity_sweep.py <traces> [auto|chunked|perround]"""
 import os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "tests"))
@@ -14,19 +14,22 @@ from paper_2506_12204_b200.tracegen import generate_batch
 from paper_2506_12204_b200.workload import WorkloadSpec
 
 T = int(sys.argv[1])
+VAR = {"auto": 0, "chunked": A.SS_FLAG_FORCE_CHUNKED, "perround": A.SS_FLAG_FORCE_PERROUND}[
+    sys.argv[2] if len(sys.argv) > 2 else "auto"]
 bad_total = 0
-for prof_name, cap, levels, n in (("a100_qwen7b", 2295, 3, 1000), ("a5000_qwen7b", 2295, 3, 1000),
-                                  ("mixed", 2295, 3, 1000), ("a100_qwen7b", 1200, 5, 800),
-                                  ("a100_qwen7b", 700, 4, 500)):
+for prof_name, cap, levels, n, b in (("a100_qwen7b", 2295, 3, 1000, 16), ("a5000_qwen7b", 2295, 3, 1000, 16),
+                                     ("mixed", 2295, 3, 1000, 16), ("a100_qwen7b", 1200, 5, 800, 16),
+                                     ("a100_qwen7b", 700, 4, 500, 16), ("a100_qwen7b", 10**9, 5, 1000, 16),
+                                     ("a100_qwen7b", 10**9, 5, 1000, 32), ("a5000_qwen7b", 10**9, 3, 2000, 8)):
     prof = MIXED_PROFILE if prof_name == "mixed" else get_profile(prof_name)
     batch = generate_batch(WorkloadSpec(total_requests=n, levels=levels), shard_seeds(T, 0, seed0=17))
-    p = lambda: make_params(prof, 16, cap, levels=levels, flags=A.SS_FLAG_DIGEST)
-    g = native.run_host(p(), batch)
+    p = lambda f=0: make_params(prof, b, cap, levels=levels, flags=A.SS_FLAG_DIGEST | f)
+    g = native.run_host(p(VAR), batch)
     c = run_oracle(p(), batch, threads=os.cpu_count())
     ok = c.stats["status"] == 0
     bad = (g.stats["status"] != c.stats["status"]) | (g.stats["rounds"] != c.stats["rounds"]) | \
           (ok & (g.stats["digest"] != c.stats["digest"]))
     bad_total += int(bad.sum())
-    print(f"{prof_name} cap {cap} levels {levels} n {n}: {T} traces, {int((~ok).sum())} ref errors, "
+    print(f"{prof_name} cap {cap} levels {levels} n {n} b {b}: {T} traces, {int((~ok).sum())} ref errors, "
           f"anomalies {int(c.stats['anomalies'].sum())}, mismatches {int(bad.sum())} {list(np.nonzero(bad)[0][:8])}")
 print("TOTAL MISMATCHES", bad_total)
