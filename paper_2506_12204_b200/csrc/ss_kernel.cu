@@ -596,7 +596,8 @@ __device__ unsigned long long g_dbg_cycles[24];
 #endif
 // sections: 0 init/admission/top, 1 fast path per-round body, 2 chunk, 3 general round, 4 outputs,
 // 5 stretch entry, 6 stretch round vote, 7 stretch order check; general round: 3 composition,
-// 8 KV admission, 9 batch duration, 10 progress, 11 record, 12 ongoing rebuild, 13 queue rebuild
+// 8 KV admission, 9 batch duration, 10 progress, 11 record, 12 ongoing rebuild, 13 queue rebuild,
+// 14 eviction calls (counter 4: evict_one calls)
 // counters: 8 chunks, 9 chunk rounds, 10 per-round fast rounds, 11 general rounds
 
 // ---- per-lane member quantities (32-bit: token counts of one request) -------
@@ -1400,12 +1401,15 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         if (lane == 0) c.dpend = 0ull;
                         __syncwarp();
                         bool ok = true;
+                        SS_SECT(14);
                         while (uni(demand + T.used > cap)) {
+                            SS_DCOUNT(4, 1);
                             if (uni(!evict_one<POL>(E, T, R, slot_k, m, mem, vcall))) {
                                 ok = false;
                                 break;
                             }
                         }
+                        SS_SECT(8);
                         const uint32_t flg_k = __shfl_sync(FULL, mem.flg, k);
                         if (uni(!ok)) {
                             // AdmissionFailure: evictions stand, their records are lost
@@ -1803,8 +1807,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     const uint32_t s = k.aux & SLOT_MASK;
                     if (s != SLOT_MASK) {
                         v = true;
-                        uint32_t* fp = FLG(A, T.off + s);
-                        *fp = *fp & ~F_INS;
+                        atomicAnd(FLG(A, T.off + s), ~F_INS);  // result unused: no round trip
                     }
                 }
                 const int2 qs = q_insert32(&A, sm, T.off, T.nF, T.nB, T.nRun, k, v);
