@@ -306,9 +306,12 @@ __device__ __noinline__ int4 refill(const KArgs* Ap, WarpSmem* sm, long long off
     const int lane = threadIdx.x & 31;
     QState T{off, nF, nB};
     Key S = kinf();  // running top-32, ascending across lanes
+    // the next chunk's load is issued before the current chunk is merged
+    Key xn = lane < T.nB ? BK(A)[T.off + lane] : kinf();
     for (int base = 0; uni(base < T.nB); base += 32) {
-        int i = base + lane;
-        Key x = i < T.nB ? BK(A)[T.off + i] : kinf();
+        Key x = xn;
+        const int in = base + 32 + lane;
+        xn = in < T.nB ? BK(A)[T.off + in] : kinf();
         Key smax = kshfl(S, 31);
         if (!__any_sync(FULL, klt(x, smax))) continue;
         x = bitonic32(x, lane, false);                 // descending
@@ -343,14 +346,14 @@ __device__ __noinline__ int4 refill(const KArgs* Ap, WarpSmem* sm, long long off
         // compact the BACK, dropping the selected keys (all <= thr)
         const unsigned lt = lanemask_lt();
         int w = 0;
+        // survivors land at or below their own index, never in the chunk loaded ahead
+        Key xn2 = lane < T.nB ? BK(A)[T.off + lane] : kinf();
         for (int base = 0; uni(base < T.nB); base += 32) {
             int i = base + lane;
-            Key x;
-            bool keep = false;
-            if (i < T.nB) {
-                x = BK(A)[T.off + i];
-                keep = klt(thr, x);
-            }
+            const Key x = xn2;
+            const int in = base + 32 + lane;
+            xn2 = in < T.nB ? BK(A)[T.off + in] : kinf();
+            const bool keep = i < T.nB && klt(thr, x);
             unsigned km = __ballot_sync(FULL, keep);
             __syncwarp();
             if (keep) BK(A)[T.off + w + __popc(km & lt)] = x;
@@ -597,7 +600,7 @@ __device__ unsigned long long g_dbg_cycles[24];
 // sections: 0 init/admission/top, 1 fast path per-round body, 2 chunk, 3 general round, 4 outputs,
 // 5 stretch entry, 6 stretch round vote, 7 stretch order check; general round: 3 composition,
 // 8 KV admission, 9 batch duration, 10 progress, 11 record, 12 ongoing rebuild, 13 queue rebuild,
-// 14 eviction calls (counter 4: evict_one calls)
+// 14 eviction calls (counter 4: evict_one calls), 15 queue refill (counter 5)
 // counters: 8 chunks, 9 chunk rounds, 10 per-round fast rounds, 11 general rounds
 
 // ---- per-lane member quantities (32-bit: token counts of one request) -------
@@ -774,6 +777,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 continue;
             }
             if (uni(T.nF < b && (T.nB > 0 || T.nRun > 0))) {
+                SS_SECT(15);
+                SS_DCOUNT(5, 1);
                 const int4 qs = refill(&A, sm, T.off, T.nF, T.nB,
                                        reinterpret_cast<const Key*>(A.w.S) + c.rbase + c.rpos, T.nRun);
                 T.nF = qs.x;
@@ -782,6 +787,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 __syncwarp();
                 if (lane == 0) c.rpos += qs.z;
                 __syncwarp();
+                SS_SECT(0);
             }
             // stale entries are transient: once none is left the trace returns to
             // the exact fast paths (checked every 32 rounds while flagged)

@@ -22,13 +22,14 @@ lib.ss_debug_cycles(buf)
 v = list(buf)
 tot = sum(v[:16]) or 1
 names = ["init/admission/top", "fast per-round body", "chunk", "g: composition", "outputs", "stretch entry", "stretch vote", "stretch order",
-         "g: KV admission", "g: batch duration", "g: progress", "g: record", "g: ongoing rebuild", "g: queue rebuild", "g: evict_one calls"]
+         "g: KV admission", "g: batch duration", "g: progress", "g: record", "g: ongoing rebuild", "g: queue rebuild", "g: evict_one calls", "refill"]
 rounds = int(res.stats["rounds"].sum())
 print(f"{W}: {T} traces, {rounds} rounds, kernel {res.kernel_ms:.2f} ms")
 for i, n in enumerate(names):
     print(f"  {n:20s} {100 * v[i] / tot:5.1f}%  {v[i] / max(rounds, 1):8.1f} warp-cycles/round")
 c = v[16:]
 print(f"  chunks {c[0]}, chunk rounds {c[1]} ({c[1] / max(c[0], 1):.1f}/chunk), per-round fast {c[2]}, general {c[3]}")
+if c[5]: print(f"  refills {c[5]}, cycles per refill {v[15] / c[5]:.0f}")
 if c[4]: print(f"  evict_one calls {c[4]}, cycles per call {v[14] / c[4]:.0f}")
 if c[0]: print(f"  cycles/chunk {v[2] / c[0]:.0f}, per chunk round {v[2] / max(c[1], 1):.0f}")
 if c[2]: print(f"  cycles per per-round fast round {v[1] / c[2]:.0f}")
