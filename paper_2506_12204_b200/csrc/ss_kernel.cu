@@ -536,13 +536,15 @@ SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot,
             log_put(c, p + 8, (uint32_t)(fa >> 32));
         }
         if (A.P.flags & SS_FLAG_DIGEST) {
-            unsigned long long r = (unsigned long long)T.rounds;
-            c.dpend += ss_term(r, SS_TAG_EV0, d, (unsigned long long)v | ((unsigned long long)action << 32));
-            c.dpend += ss_term(r, SS_TAG_EV1, d,
-                               (unsigned long long)(uint32_t)saved | ((unsigned long long)(uint32_t)discarded << 32));
-            c.dpend += ss_term(r, SS_TAG_EV2, d, (unsigned long long)freed);
-            c.dpend += ss_term(r, SS_TAG_EV3, d, dbits(ftb));
-            c.dpend += ss_term(r, SS_TAG_EV4, d, dbits(fta));
+            const unsigned long long r = (unsigned long long)T.rounds;
+            const unsigned long long w0 = (unsigned long long)v | ((unsigned long long)action << 32),
+                                     w1 = (unsigned long long)(uint32_t)saved | ((unsigned long long)(uint32_t)discarded << 32),
+                                     w2 = (unsigned long long)freed, w3 = dbits(ftb), w4 = dbits(fta);
+#pragma unroll 1
+            for (int f = 0; f < 5; f++) {  // one copy of the hash
+                const unsigned long long val = f == 0 ? w0 : (f == 1 ? w1 : (f == 2 ? w2 : (f == 3 ? w3 : w4)));
+                c.dpend += ss_term(r, SS_TAG_EV0 + (uint32_t)f, d, val);
+            }
         }
         c.s_victims += 1;
     }
@@ -941,11 +943,21 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             val = (lane == 31) ? hv : val;
                             // ss_term(r, tag, 0, val) with ((r << 24) ^ c) * G = r * (G << 24) + c * G
                             // (c < 2^24): the round part advances by one add per round
-                            const unsigned long long term = ss_mix64(val ^ (dgr + dgc));
-                            dig += hl ? term : 0ull;
+                            // completion terms share the hash pass with the header lanes; a
+                            // completing header lane (b > 29) takes a second pass
+                            const bool dn = (cdm >> lane) & 1u;
+                            const unsigned long long dx =
+                                (unsigned long long)mem.slot ^
+                                (((r64 << 24) ^ ((unsigned long long)SS_TAG_DONE << 20) ^ (unsigned long long)__popc(cdm & lt)) *
+                                 0x9E3779B97F4A7C15ull);
                             dig += act ? gt * rmul : 0ull;
-                            if (cround && ((cdm >> lane) & 1u))
-                                dig += ss_term(r64, SS_TAG_DONE, __popc(cdm & lt), mem.slot);
+                            const int passes = 1 + (__any_sync(FULL, dn && hl) ? 1 : 0);
+#pragma unroll 1
+                            for (int ps = 0; ps < passes; ps++) {
+                                const bool hdr = ps == 0 && hl, use = hdr || (dn && (ps == 1) == hl);
+                                const unsigned long long term = ss_mix64(hdr ? (val ^ (dgr + dgc)) : dx);
+                                dig += use ? term : 0ull;
+                            }
                         }
                         dgr += DG24;
                         rmul += 2u * SS_DG_ROUND;
@@ -1512,10 +1524,10 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             if (uni(ng == 0)) {
                 // nothing granted (engine.py:329-344): clock does not advance
                 T.nO = 0;
-                if (want_digest && lane == 0) {
-                    dig += ss_term(r64, SS_TAG_HDR, 0, ss_hdr_word(SS_KIND_NONE, 0, 0, R.ndec));
-                    dig += ss_term(r64, SS_TAG_MEM, 0, (unsigned long long)T.used);
-                    dig += ss_term(r64, SS_TAG_TIME, 0, dbits(T.clock));
+                if (want_digest && lane < 3) {  // header / memory / time, one lane each
+                    const unsigned long long val = lane == 0 ? ss_hdr_word(SS_KIND_NONE, 0, 0, R.ndec)
+                                                             : (lane == 1 ? (unsigned long long)T.used : dbits(T.clock));
+                    dig += ss_term(r64, lane == 0 ? SS_TAG_HDR : (lane == 1 ? SS_TAG_MEM : SS_TAG_TIME), 0, val);
                 }
                 if (R.ndec > 0 && lane == 0) {
                     if (T.used > peak) peak = T.used;
@@ -1741,15 +1753,23 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     const unsigned long long hval =
                         lane == 31 ? ss_hdr_word(kind, ng, nc_done, R.ndec)
                                    : (lane == 30 ? (unsigned long long)T.used : dbits(end));
-                    if (g_act || hl) {  // one mix per lane: grant term or ss_term(r, htag, 0, hval)
+                    // up to three passes through one copy of the hash: 0 grant term (granted
+                    // lanes) or header term (lanes 29..31); 1 header term of granted lanes
+                    // 29..31 (b > 29); 2 completion terms
+                    const unsigned long long hsalt = ((r64 << 24) ^ ((unsigned long long)htag << 20)) * 0x9E3779B97F4A7C15ull;
+                    const unsigned long long dsalt = ((r64 << 24) ^ ((unsigned long long)SS_TAG_DONE << 20) ^
+                                                      (unsigned long long)ci) * 0x9E3779B97F4A7C15ull;
+#pragma unroll 1
+                    for (int ps = 0; ps < 3; ps++) {
+                        const bool use = ps == 0 ? (g_act || hl) : (ps == 1 ? (m > 29 && hl && g_act) : (done && cdone != 0));
+                        if (!__any_sync(FULL, use)) continue;
+                        const bool grant = ps == 0 && g_act;
                         const unsigned long long x =
-                            g_act ? ((unsigned long long)mem.slot ^ ((unsigned long long)(gi + 1) * SS_DG_POS))
-                                  : (hval ^ (((r64 << 24) ^ ((unsigned long long)htag << 20)) * 0x9E3779B97F4A7C15ull));
+                            grant ? ((unsigned long long)mem.slot ^ ((unsigned long long)(gi + 1) * SS_DG_POS))
+                                  : (ps == 2 ? ((unsigned long long)mem.slot ^ dsalt) : (hval ^ hsalt));
                         const unsigned long long h = ss_mix64(x);
-                        dig += g_act ? h * ss_round_mul(r64) : h;
+                        dig += use ? (grant ? h * ss_round_mul(r64) : h) : 0ull;
                     }
-                    if (m > 29 && hl && g_act) dig += ss_term(r64, htag, 0, hval);
-                    if (cdone && done) dig += ss_term(r64, SS_TAG_DONE, ci, mem.slot);
                 }
                 if (logging) {
                     const long long lp = c.logpos;
