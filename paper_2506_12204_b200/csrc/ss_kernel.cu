@@ -439,7 +439,7 @@ __device__ void q_delete(const Env& E, Trace& T, Round& R, uint32_t v, uint32_t 
 // Evict one victim for member `kslot` (kvcache.py:160-175): the resident with
 // the largest dispatch key that is neither granted this round nor `kslot`.
 // Returns false if there is none (AdmissionFailure). Cold path: not inlined.
-template <int POL>
+template <int POL, bool LOGGING>
 SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot, int m, MemS& mem,
                                        unsigned& vcall) {
     const KArgs& A = *E.A;
@@ -522,7 +522,7 @@ SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot,
         store_dyn(A, gv, fta, (uint32_t)saved, nflg);
         A.out.req.evictions[gv] += 1u;
         const int d = R.ndec;  // decision record: kept only if the admission succeeds
-        if (c.log) {
+        if (LOGGING && c.log) {  // compile-time: no log code in the digest-only kernels
             long long p = c.logpos + SS_LOG_HEADER_WORDS + (long long)SS_LOG_DECISION_WORDS * d;
             unsigned long long fb = dbits(ftb), fa = dbits(fta);
             log_put(c, p + 0, v);
@@ -1438,7 +1438,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         SS_SECT(14);
                         while (uni(demand + T.used > cap)) {
                             SS_DCOUNT(4, 1);
-                            if (uni(!evict_one<POL>(E, T, R, slot_k, m, mem, vcall))) {
+                            if (uni(!evict_one<POL, logging>(E, T, R, slot_k, m, mem, vcall))) {
                                 ok = false;
                                 break;
                             }
@@ -1531,7 +1531,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 }
                 if (R.ndec > 0 && lane == 0) {
                     if (T.used > peak) peak = T.used;
-                    if (c.log) {
+                    if (logging && c.log) {
                         const unsigned long long mu = (unsigned long long)T.used, tb = dbits(T.clock);
                         log_put(c, c.logpos + 0, SS_KIND_NONE);
                         log_put(c, c.logpos + 1, 0);
