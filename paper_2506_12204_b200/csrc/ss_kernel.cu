@@ -850,12 +850,19 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         safe_used = cap - (long long)maxdem - m;
                         gt = act ? ss_grant_term((uint32_t)lane, mem.slot) : 0ull;
                     };
-                    setup();
+                    // chunked kernels: one call site (one copy of its code) at the loop top;
+                    // per-round kernels call it directly (no extra vote per round)
+                    bool need_setup = chunking;
+                    if (!chunking) setup();
                     int k = 0;
                     long long spool = 0, sgr = 0;  // live and granted requests summed over the rounds
                     int live_s = live;
                     for (;;) {
                         SS_SECT(6);
+                        if (chunking && uni(need_setup)) {
+                            setup();
+                            need_setup = false;
+                        }
                         // one vote for every exit: a completion, an admission due, p*
                         // queued (no ongoing key below the queue front), round cap / log
                         const bool adm = T.next_ready <= ss::add(T.clock, 1e-12);
@@ -1017,7 +1024,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             T.nO = m;
                             live_s -= ncd;
                             if (uni(m == 0)) break;
-                            setup();
+                            if (chunking) need_setup = true;
+                            else setup();
                         }
                         SS_SECT(7);
                         // the ongoing set stays sorted by key (usually already is)
