@@ -655,11 +655,15 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
     // back to back; the one the prepass did not select (ss_prepass.cu
     // select_kernel: chunks only when the KV budget can never bind) exits at once.
     constexpr bool chunking = (MODE & 4) != 0;
+    // MODE bit 3 (with bit 2): no trace can ever evict (select_kernel's footprint rule).
+    // The eviction path, the stale-entry (anomaly) handling it can cause and the
+    // resident list (eviction candidates) are compiled out: a denser hot loop.
+    constexpr bool noev = (MODE & 8) != 0;
     const int sel = *A.w.sel;
-    if (POL == SS_POLICY_SEMANTIC && (sel != SS_SEL_PERROUND) != chunking) return;
-    // no trace can ever evict (select_kernel's footprint rule): the resident list
-    // (eviction candidates) is never read, so it is not maintained
-    const bool track_res = sel != SS_SEL_NO_EVICT;
+    if (POL == SS_POLICY_SEMANTIC &&
+        sel != (noev ? SS_SEL_NO_EVICT : (chunking ? SS_SEL_CHUNKED : SS_SEL_PERROUND)))
+        return;
+    const bool track_res = !noev;
 #ifdef SS_DEBUG_TIMING
     unsigned long long dbg_acc[24] = {0};
     long long dbg_t = clock64();
@@ -1421,7 +1425,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     const unsigned qa = __ballot_sync(FULL, ((R.G >> lane) & 1u) && (mem.flg & F_Q));
                     if (qa && lane == 0) c.anomalies += __popc(qa);
                 }
-                if (nm) {
+                if (noev && nm) set_status(T, SS_TRACE_INTERNAL);  // the footprint rule excludes this
+                if (!noev && nm) {
                     if (lane == 0) c.s_res += T.nR;
                     // slow path: one member at a time from the first that must evict
                     long long reserved = __shfl_sync(FULL, excl, f);
@@ -2011,7 +2016,12 @@ static const void* kernel_ptr(int mode) {
     case 4: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 4> : nullptr;
     case 5: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 5> : nullptr;
     case 6: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 6> : nullptr;
-    default: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 7> : nullptr;
+    case 7: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 7> : nullptr;
+    // chunked stretches, no eviction possible
+    case 12: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 12> : nullptr;
+    case 13: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 13> : nullptr;
+    case 14: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 14> : nullptr;
+    default: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 15> : nullptr;
     }
 }
 
@@ -2043,16 +2053,18 @@ int launch_sched(const KArgs& a, int blocks, void* stream) {
     const void* k = kernel_for(a.P.policy, mode_of(a.P.flags));
     if (!k) return SS_ERR_UNSUPPORTED;
     void* argv[] = {(void*)&a};
-    if (a.P.policy == SS_POLICY_SEMANTIC) {  // the chunked variant first; the unselected one exits at once
-        const void* kc = kernel_for(a.P.policy, mode_of(a.P.flags) | 4);
-        cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (cudaLaunchKernel(kc, dim3(blocks), dim3(32 * WPB), argv, smem, st) != cudaSuccess) return SS_ERR_CUDA;
+    if (a.P.policy == SS_POLICY_SEMANTIC) {  // the chunked variants first; the unselected ones exit at once
+        for (int v : {12, 4}) {
+            const void* kc = kernel_for(a.P.policy, mode_of(a.P.flags) | v);
+            cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (cudaLaunchKernel(kc, dim3(blocks), dim3(32 * WPB), argv, smem, st) != cudaSuccess) return SS_ERR_CUDA;
+        }
     }
     if (cudaLaunchKernel(k, dim3(blocks), dim3(32 * WPB), argv, smem, st) != cudaSuccess) return SS_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? SS_OK : SS_ERR_CUDA;
 }
 
-int sched_launches(int policy) { return policy == SS_POLICY_SEMANTIC ? 2 : 1; }
+int sched_launches(int policy) { return policy == SS_POLICY_SEMANTIC ? 3 : 1; }
 
 }  // namespace ss
 

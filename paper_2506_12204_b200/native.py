@@ -73,8 +73,9 @@ def launches_per_run(params=None, max_trace_len=None) -> int:
     if params is not None and max_trace_len is not None:
         bulk = _bulk_possible(params, max_trace_len)
     # detect, scan, init, select (+ the bulk sort) + the scheduler: semantic runs
-    # launch the chunked and the per-round variant, the unselected one exits at once
-    sched = 2 if params is None or params.policy == A.SS_POLICY["semantic"] else 1
+    # launch the three variants (chunked without eviction, chunked, per-round); the
+    # unselected ones exit at once
+    sched = 3 if params is None or params.policy == A.SS_POLICY["semantic"] else 1
     return 4 + (3 + 16 * 3 + 1 if bulk else 0) + sched
 
 
