@@ -849,9 +849,13 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         nmax = __reduce_max_sync(FULL, act ? m_prompt(mem) + mem.dec + 1u : 0u);
                         // KV admission (engine.py:296-327) of an all-decode batch: immediate 1,
                         // exclusive scan = lane, demand = max(est, 1), est non-increasing
-                        const long long est0 = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
-                        const int maxdem = (int)__reduce_max_sync(FULL, (unsigned)(est0 > 1 ? est0 : 1));
-                        safe_used = cap - (long long)maxdem - m;
+                        if (noev) {
+                            safe_used = 0x7fffffffffffffffll;  // no eviction possible
+                        } else {
+                            const long long est0 = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
+                            const int maxdem = (int)__reduce_max_sync(FULL, (unsigned)(est0 > 1 ? est0 : 1));
+                            safe_used = cap - (long long)maxdem - m;
+                        }
                         gt = act ? ss_grant_term((uint32_t)lane, mem.slot) : 0ull;
                     };
                     // chunked kernels: one call site (one copy of its code) at the loop top;
@@ -878,7 +882,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             if (!uni((left <= 0) & !adm & !capx) || !__any_sync(FULL, pdec)) break;
                             cround = true;
                         }
-                        if (uni(T.used > safe_used)) {
+                        if (!noev && uni(T.used > safe_used)) {
                             long long e = (long long)m_mid(mem) - (long long)mem.dec;
                             long long dem = e > 1 ? e : 1;
                             if (dem + lane > cap) dem = 1;
@@ -898,7 +902,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
 #ifndef SS_NO_CHUNK
                         if (chunking && !cround && !sum_mode) {
                             chunk = left >= SS_CHUNK_MIN && T.rounds + (SS_CHUNK_MIN - 1) < round_cap &&
-                                    T.used + (long long)(SS_CHUNK_MIN - 1) * m <= safe_used;
+                                    (noev || T.used + (long long)(SS_CHUNK_MIN - 1) * m <= safe_used);
                             if (logging)
                                 chunk = chunk && c.logpos + (long long)(SS_CHUNK_MIN - 1) * (SS_LOG_HEADER_WORDS + m) <=
                                                      c.logcap;
@@ -1104,8 +1108,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             // ongoing, no admission is due at its start and no static bound
                             // (completion, round cap, memory safety, log space) stops it
                             const bool adm_j = T.next_ready <= ss::add(befj, 1e-12);
-                            bool lim = (lane >= L) | (T.rounds + lane >= round_cap) |
-                                       (T.used + (long long)lane * m > safe_used);
+                            bool lim = (lane >= L) | (T.rounds + lane >= round_cap);
+                            if (!noev) lim |= T.used + (long long)lane * m > safe_used;
                             if (logging) lim |= c.logpos + (long long)lane * (SS_LOG_HEADER_WORDS + m) > c.logcap;
                             const unsigned stop = __ballot_sync(FULL, lim | adm_j) |
                                                   (__ballot_sync(FULL, !(pk & ok)) << 1);
