@@ -908,7 +908,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                                      c.logcap;
                         }
 #endif
-                        if (!chunking || uni(!chunk)) {  // one round here; the chunk below is laid out after the loop's hot path
+                        if (!chunking || uni(!chunk)) {  // one round here
                         double part;  // batch_duration (engine.py:126-149) of an all-decode batch
                         SS_SECT(1);
                         SS_DCOUNT(2, 1);
@@ -1035,35 +1035,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             if (chunking) need_setup = true;
                             else setup();
                         }
-                        SS_SECT(7);
-                        // the ongoing set stays sorted by key (usually already is)
-                        okey = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, true);
-                        Key nx;  // order check needs the next lane's (hi, lo) only
-                        nx.hi = __shfl_down_sync(FULL, okey.hi, 1);
-                        nx.lo = __shfl_down_sync(FULL, okey.lo, 1);
-                        const bool reord = uni(__ballot_sync(FULL, (lane + 1 < m) & klt_nb(nx, okey)) != 0u);
-                        if (reord) {
-                            if (act) sm->X[32 + lane] = okey;
-                            __syncwarp();
-                            int r = 0;
-                            for (int q = 0; uni(q < m); q++) r += klt(sm->X[32 + q], okey) ? 1 : 0;
-                            __syncwarp();
-                            if (act) {
-                                sm->OM[r] = mem;
-                                sm->X[32 + r] = okey;
-                            }
-                            __syncwarp();
-                            if (act) {
-                                mem = sm->OM[lane];
-                                okey = sm->X[32 + lane];
-                            }
-                            __syncwarp();
-                        }
-                        if (reord) break;  // positions moved: the next stretch recomputes the grant terms
-                            continue;
                         }
 #ifndef SS_NO_CHUNK
-                        {
+                        else {
                             SS_SECT(2);
                             const int L = left < 32 ? left : 32;
                             if (act) sm->OM[lane] = mem;  // broadcast source of the member loop
@@ -1168,6 +1142,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             if (lft < 1) lft = 1;
                             mem.ft = ss::add(z0, decode_total_time((long long)m_prompt(mem) + mem.dec, lft, P));
                         }
+#endif
                         SS_SECT(7);
                         // the ongoing set stays sorted by key (usually already is)
                         okey = make_key<POL>(m_rank(mem), mem.ft, m_tie(mem), mem.slot, true);
@@ -1193,7 +1168,6 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             __syncwarp();
                         }
                         if (reord) break;  // positions moved: the next stretch recomputes the grant terms
-#endif
                     }
                     if (uni(T.rounds >= round_cap)) set_status(T, SS_TRACE_ROUND_CAP);
                     if (logging && uni(c.logpos > c.logcap)) set_status(T, SS_TRACE_LOG_OVERFLOW);
