@@ -659,6 +659,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
     // The eviction path, the stale-entry (anomaly) handling it can cause and the
     // resident list (eviction candidates) are compiled out: a denser hot loop.
     constexpr bool noev = (MODE & 8) != 0;
+    // MODE bit 4 (no-eviction kernels only): decode_batch_cost "sum" compiled in; the
+    // other no-eviction kernels carry only the "max" batch duration
+    constexpr bool sum_k = (MODE & 16) != 0;
     const int sel = *A.w.sel;
     if (POL == SS_POLICY_SEMANTIC &&
         sel != (noev ? SS_SEL_NO_EVICT : (chunking ? SS_SEL_CHUNKED : SS_SEL_PERROUND)))
@@ -832,7 +835,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     // remaining_time of a decoding member (costs.py:174-191): reload(0)
                     // and prefill(0) are the same constants every round
                     const double z0 = ss::add(reload_time(0, P), prefill_time(0, P));
-                    const bool sum_mode = A.P.decode_cost_sum != 0;
+                    const bool sum_mode = noev ? sum_k : A.P.decode_cost_sum != 0;
                     constexpr unsigned long long DG = 0x9E3779B97F4A7C15ull, DG24 = DG << 24;
                     unsigned long long dgr = (unsigned long long)T.rounds * DG24;
                     // per-membership values, recomputed when members complete
@@ -1558,7 +1561,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 const unsigned dm = __ballot_sync(FULL, g_act && q.isdec);
                 if (dm) {
                     double part;
-                    if (uni(!A.P.decode_cost_sum)) {
+                    if (noev ? !sum_k : uni(!A.P.decode_cost_sum)) {
                         // gamma1 >= 0: the step time is monotone in the context length,
                         // so the max step is the step of the longest context
                         const unsigned nmax =
@@ -1999,7 +2002,12 @@ static const void* kernel_ptr(int mode) {
     case 12: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 12> : nullptr;
     case 13: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 13> : nullptr;
     case 14: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 14> : nullptr;
-    default: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 15> : nullptr;
+    case 15: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 15> : nullptr;
+    // ... with decode_batch_cost "sum"
+    case 28: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 28> : nullptr;
+    case 29: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 29> : nullptr;
+    case 30: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 30> : nullptr;
+    default: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 31> : nullptr;
     }
 }
 
@@ -2032,7 +2040,7 @@ int launch_sched(const KArgs& a, int blocks, void* stream) {
     if (!k) return SS_ERR_UNSUPPORTED;
     void* argv[] = {(void*)&a};
     if (a.P.policy == SS_POLICY_SEMANTIC) {  // the chunked variants first; the unselected ones exit at once
-        for (int v : {12, 4}) {
+        for (int v : {a.P.decode_cost_sum ? 28 : 12, 4}) {
             const void* kc = kernel_for(a.P.policy, mode_of(a.P.flags) | v);
             cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (cudaLaunchKernel(kc, dim3(blocks), dim3(32 * WPB), argv, smem, st) != cudaSuccess) return SS_ERR_CUDA;
