@@ -5,10 +5,10 @@
 # 2) one `ncu --set full` capture of the scheduler kernel (source-level stalls).
 # Semantic runs launch two scheduler variants and the unselected one exits at
 # once: the regex names the selected one by its mangled name, e.g.
-# sched_kernelILi0ELi5E (semantic, digest, chunked; config B/E) or
+# sched_kernelILi0ELi13E (semantic, digest, chunked, no eviction; config B/E), ILi0ELi5E (chunked, evicting; forced) or
 # sched_kernelILi0ELi1E (semantic, digest, per-round; config D).
 set -u
-W=${1:-B}; R=${2:-r01}; K=${3:-sched_kernelILi0ELi5E}
+W=${1:-B}; R=${2:-r01}; K=${3:-sched_kernelILi0ELi13E}
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/ncu_launches_${W}_${R}.csv \
