@@ -662,6 +662,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
     // MODE bit 4 (no-eviction kernels only): decode_batch_cost "sum" compiled in; the
     // other no-eviction kernels carry only the "max" batch duration
     constexpr bool sum_k = (MODE & 16) != 0;
+    constexpr bool anom_ok = !noev;  // stale heap entries can arise (an eviction can lose its decisions)
     const int sel = *A.w.sel;
     if (POL == SS_POLICY_SEMANTIC &&
         sel != (noev ? SS_SEL_NO_EVICT : (chunking ? SS_SEL_CHUNKED : SS_SEL_PERROUND)))
@@ -810,7 +811,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             // stale entries are transient: once none is left the trace returns to
             // the exact fast paths (checked every 32 rounds while flagged)
 #ifndef SS_NO_ANOM_EXIT
-            if (!noev && uni(anom && (T.rounds & 31) == 0) &&
+            if (anom_ok && uni(anom && (T.rounds & 31) == 0) &&
                 !queue_has_stale<POL>(&A, sm, T.off, T.nF, T.nB, T.nO))
                 anom = false;
 #endif
@@ -822,7 +823,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             // members in registers, record writes deferred to the stretch's end and
             // the same arithmetic, digest terms and bookkeeping as the general
             // round below (engine.py:288-380), which handles every other round.
-            if (POL == SS_POLICY_SEMANTIC && uni((noev || !anom) && T.nO > 0 && T.nO <= b)) {
+            if (POL == SS_POLICY_SEMANTIC && uni((!anom_ok || !anom) && T.nO > 0 && T.nO <= b)) {
                 SS_SECT(5);
                 const int nc0 = T.nF < b ? T.nF : b;
                 const bool cdec = lane < nc0 && (sm->F[lane].aux & DEC_BIT);
@@ -1208,7 +1209,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             Key ck;  // candidate key: stored (fast path) or current (general path)
             if (has_c) {
                 ck = sm->F[lane];
-                if (!noev && anom) {
+                if (anom_ok && anom) {
                     MemS cm;
                     load_mem(A, T.off, ck.aux & SLOT_MASK, cm);
                     ck = mem_key<POL>(cm);
@@ -1219,7 +1220,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             // in the reference: equal keys are copies of the same request)
             Key pmin = kinf();
             if (POL != SS_POLICY_SEMANTIC) {
-            } else if (noev || uni(!anom)) {
+            } else if (!anom_ok || uni(!anom)) {
                 if (T.nO > 0) pmin = sm->X[32];
                 if (nc > 0 && klt(sm->F[0], pmin)) pmin = sm->F[0];
             } else {
@@ -1243,7 +1244,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 // ongoing first in their order, then the popped candidates
                 cnt_o = lane;
                 cnt_c = T.nO + lane;
-            } else if (noev || uni(!anom)) {
+            } else if (!anom_ok || uni(!anom)) {
                 // both lists sorted: rank = own index + lower_bound in the other
                 cnt_o = lane;
                 if (cmask) {
@@ -1300,7 +1301,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             if (c_sel) {
                 MemS cm;
                 load_mem(A, T.off, ck.aux & SLOT_MASK, cm);
-                if (!noev && anom) {  // another copy may have moved the flags: re-read them
+                if (anom_ok && anom) {  // another copy may have moved the flags: re-read them
                     cm.flg = flg_update(A, T.off + cm.slot, F_Q, 0u);  // popped from the heap for good
                 } else {  // distinct requests: the loaded flags are current
                     cm.flg &= ~F_Q;
@@ -1309,7 +1310,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 sm->M[cnt_c] = cm;
             }
             if (!direct && has_o && cnt_o < m) sm->M[cnt_o] = sm->OM[lane];
-            if (!noev && uni(anom)) {
+            if (anom_ok && uni(anom)) {
                 // candidates not selected are pushed back with their current key;
                 // a stale stored key is replaced (heaps.py insert after pop)
                 const bool refresh = has_c && !c_sel && !keq(ck, sm->F[lane]);
@@ -1362,7 +1363,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             const bool act = lane < m;
             if (act) {
                 mem = direct ? sm->OM[lane] : sm->M[lane];
-                if (!noev && anom) mem.flg = *FLG(A, T.off + mem.slot);  // queued bit may have moved
+                if (anom_ok && anom) mem.flg = *FLG(A, T.off + mem.slot);  // queued bit may have moved
             }
             if (POL != SS_POLICY_SEMANTIC) {
                 // BatchKind from the selected members' stages (engine.py:263-267, 280-284)
@@ -1371,7 +1372,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             const int nO_start = T.nO;
             const int nuns_start = c.nuns;
             // a completed request popped from a stale entry: estimate_kv_size raises
-            if (!noev && uni(anom) && __ballot_sync(FULL, act && (mem.flg & F_STAGE) == ST_DONE)) {
+            if (anom_ok && uni(anom) && __ballot_sync(FULL, act && (mem.flg & F_STAGE) == ST_DONE)) {
                 set_status(T, SS_TRACE_REF_ERROR);
                 T.rounds += 1;
                 break;
@@ -1401,7 +1402,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 const unsigned mmask = m >= 32 ? FULL : ((1u << m) - 1u);
                 const int f = nm ? __ffs(nm) - 1 : m;
                 R.G = (f >= 32 ? FULL : ((1u << f) - 1u)) & mmask;
-                if (!noev && uni(anom)) {
+                if (anom_ok && uni(anom)) {
                     // grants of still-queued requests (stale heap entry) before f
                     const unsigned qa = __ballot_sync(FULL, ((R.G >> lane) & 1u) && (mem.flg & F_Q));
                     if (qa && lane == 0) c.anomalies += __popc(qa);
@@ -1497,7 +1498,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 }
             }
             if (uni(T.status != SS_TRACE_OK)) break;
-            if (!noev && uni(anom)) {
+            if (anom_ok && uni(anom)) {
                 // copies of one request must agree before duration and execution
                 __syncwarp();
                 if (act) {
@@ -1587,7 +1588,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 SS_SECT(10);
                 bool done = false;
                 bool dups = false;
-                if (!noev && uni(anom)) {
+                if (anom_ok && uni(anom)) {
                     const unsigned dupm = __match_any_sync(FULL, g_act ? mem.slot : (0x80000000u | lane));
                     dups = __ballot_sync(FULL, g_act && __popc(dupm) > 1) != 0;
                 }
