@@ -322,7 +322,25 @@ __device__ __noinline__ int4 refill(const KArgs* Ap, WarpSmem* sm, long long off
         const int in = base + 32 + lane;
         xn = in < T.nB ? BK(A)[T.off + in] : kinf();
         Key smax = kshfl(S, 31);
-        if (!__any_sync(FULL, klt(x, smax))) continue;
+        unsigned qm = __ballot_sync(FULL, klt(x, smax));
+        if (!qm) continue;
+        if (__popc(qm) <= 6) {
+            // few keys beat the running 32nd: insert them one by one (rank by ballot,
+            // shift the larger entries up one lane, the largest drops out)
+            while (qm) {
+                const int src = __ffs(qm) - 1;
+                qm &= qm - 1;
+                const Key y = kshfl(x, src);
+                const int pos = __popc(__ballot_sync(FULL, klt(S, y)));
+                Key up;
+                up.hi = __shfl_up_sync(FULL, S.hi, 1);
+                up.lo = __shfl_up_sync(FULL, S.lo, 1);
+                up.aux = __shfl_up_sync(FULL, S.aux, 1);
+                if (lane > pos) S = up;
+                else if (lane == pos) S = y;
+            }
+            continue;
+        }
         x = bitonic32(x, lane, false);                 // descending
         if (klt(x, S)) S = x;                          // bitonic sequence
 #pragma unroll
