@@ -203,6 +203,11 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
     S = S < 1 ? 1 : (S > SS_MAX_SLICES ? SS_MAX_SLICES : S);
     int32_t t0s[SS_MAX_SLICES + 1];
     for (int s = 0; s <= S; s++) t0s[s] = (int32_t)((int64_t)T * s / S);
+    if (S == 4) {  // small first / last slices: compute starts sooner, the last download is shorter
+        t0s[1] = T / 8;
+        t0s[2] = T / 2;
+        t0s[3] = T - T / 8;
+    }
     size_t in_b = 2 * a16((size_t)(n > 0 ? n : 1) * 8) + 4 * a16((size_t)(n > 0 ? n : 1) * 4) +
                   2 * a16((size_t)(n > 0 ? n : 1));
     const size_t nn = (size_t)(n > 0 ? n : 1);
