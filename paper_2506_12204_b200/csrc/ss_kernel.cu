@@ -677,8 +677,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
     // The eviction path, the stale-entry (anomaly) handling it can cause and the
     // resident list (eviction candidates) are compiled out: a denser hot loop.
     constexpr bool noev = (MODE & 8) != 0;
-    // MODE bit 4 (no-eviction kernels only): decode_batch_cost "sum" compiled in; the
-    // other no-eviction kernels carry only the "max" batch duration
+    // MODE bit 4: decode_batch_cost "sum" (Neumaier sum of the members' decode steps)
+    // compiled in; the other kernels carry only the "max" batch duration
     constexpr bool sum_k = (MODE & 16) != 0;
     constexpr bool anom_ok = !noev;  // stale heap entries can arise (an eviction can lose its decisions)
     const int sel = *A.w.sel;
@@ -854,7 +854,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     // remaining_time of a decoding member (costs.py:174-191): reload(0)
                     // and prefill(0) are the same constants every round
                     const double z0 = ss::add(reload_time(0, P), prefill_time(0, P));
-                    const bool sum_mode = noev ? sum_k : A.P.decode_cost_sum != 0;
+                    constexpr bool sum_mode = sum_k;
                     constexpr unsigned long long DG = 0x9E3779B97F4A7C15ull, DG24 = DG << 24;
                     unsigned long long dgr = (unsigned long long)T.rounds * DG24;
                     // per-membership values, recomputed when members complete
@@ -1580,7 +1580,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 const unsigned dm = __ballot_sync(FULL, g_act && q.isdec);
                 if (dm) {
                     double part;
-                    if (noev ? !sum_k : uni(!A.P.decode_cost_sum)) {
+                    if (!sum_k) {
                         // gamma1 >= 0: the step time is monotone in the context length,
                         // so the max step is the step of the longest context
                         const unsigned nmax =
@@ -2005,30 +2005,28 @@ static int mode_of(uint32_t flags) {
     return ((flags & SS_FLAG_DIGEST) ? 1 : 0) | ((flags & SS_FLAG_ROUND_LOG) ? 2 : 0);
 }
 
+// MODE bits: 0 digest, 1 round log, 2 chunked stretches (semantic), 3 no eviction
+// possible (with 2), 4 "sum" batch durations
+#define SS_K(M) \
+    case M: return (const void*)sched_kernel<POL, M>;
 template <int POL>
 static const void* kernel_ptr(int mode) {
-    switch (mode) {
-    case 0: return (const void*)sched_kernel<POL, 0>;
-    case 1: return (const void*)sched_kernel<POL, 1>;
-    case 2: return (const void*)sched_kernel<POL, 2>;
-    case 3: return (const void*)sched_kernel<POL, 3>;
-    // chunked-stretch variants: the fast path exists for the semantic policy only
-    case 4: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 4> : nullptr;
-    case 5: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 5> : nullptr;
-    case 6: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 6> : nullptr;
-    case 7: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 7> : nullptr;
-    // chunked stretches, no eviction possible
-    case 12: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 12> : nullptr;
-    case 13: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 13> : nullptr;
-    case 14: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 14> : nullptr;
-    case 15: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 15> : nullptr;
-    // ... with decode_batch_cost "sum"
-    case 28: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 28> : nullptr;
-    case 29: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 29> : nullptr;
-    case 30: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 30> : nullptr;
-    default: return POL == SS_POLICY_SEMANTIC ? (const void*)sched_kernel<POL, 31> : nullptr;
+    if constexpr (POL == SS_POLICY_SEMANTIC) {
+        switch (mode) {
+            SS_K(0) SS_K(1) SS_K(2) SS_K(3) SS_K(4) SS_K(5) SS_K(6) SS_K(7)
+            SS_K(12) SS_K(13) SS_K(14) SS_K(15)
+            SS_K(16) SS_K(17) SS_K(18) SS_K(19) SS_K(20) SS_K(21) SS_K(22) SS_K(23)
+            SS_K(28) SS_K(29) SS_K(30) SS_K(31)
+        default: return nullptr;
+        }
+    } else {  // the stretch / chunk fast paths exist for the semantic policy only
+        switch (mode) {
+            SS_K(0) SS_K(1) SS_K(2) SS_K(3) SS_K(16) SS_K(17) SS_K(18) SS_K(19)
+        default: return nullptr;
+        }
     }
 }
+#undef SS_K
 
 static const void* kernel_for(int policy, int mode) {
     switch (policy) {
@@ -2055,12 +2053,13 @@ int sched_max_blocks(int policy, int* sm_count) {
 int launch_sched(const KArgs& a, int blocks, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     size_t smem = (size_t)sched_smem_bytes();
-    const void* k = kernel_for(a.P.policy, mode_of(a.P.flags));
+    const int mode = mode_of(a.P.flags) | (a.P.decode_cost_sum ? 16 : 0);
+    const void* k = kernel_for(a.P.policy, mode);
     if (!k) return SS_ERR_UNSUPPORTED;
     void* argv[] = {(void*)&a};
     if (a.P.policy == SS_POLICY_SEMANTIC) {  // the chunked variants first; the unselected ones exit at once
-        for (int v : {a.P.decode_cost_sum ? 28 : 12, 4}) {
-            const void* kc = kernel_for(a.P.policy, mode_of(a.P.flags) | v);
+        for (int v : {12, 4}) {
+            const void* kc = kernel_for(a.P.policy, mode | v);
             cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (cudaLaunchKernel(kc, dim3(blocks), dim3(32 * WPB), argv, smem, st) != cudaSuccess) return SS_ERR_CUDA;
         }
