@@ -281,6 +281,9 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
         for (int s = 0; s < S; s++) CK(cudaEventCreate(&ev_k1[s]));
     }
     size_t ooff = 0, wsoff = 0;
+    ss_outputs so_s[SS_MAX_SLICES];
+    int64_t ra_s[SS_MAX_SLICES], ns_s[SS_MAX_SLICES], la_s[SS_MAX_SLICES], lw_s[SS_MAX_SLICES];
+    int32_t ta_s[SS_MAX_SLICES], Ts_s[SS_MAX_SLICES];
     for (int s = 0; s < S; s++) {
         cudaStream_t st = g_stage.streams[s];
         CK(cudaStreamWaitEvent(st, ev_in, 0));
@@ -348,9 +351,24 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
         if (rc) return rc;
         wsoff += a16(wsz);
         if (ev_k0) CK(cudaEventRecord(ev_k1[s], st));
+        so_s[s] = so;
+        ra_s[s] = ra;
+        ns_s[s] = ns;
+        ta_s[s] = ta;
+        Ts_s[s] = Ts;
+        la_s[s] = la;
+        lw_s[s] = lw;
+    }
+    // downloads only after every slice's work is queued: a pageable destination makes
+    // cudaMemcpyAsync block the host, which must not delay the later slices' uploads
+    for (int s = 0; s < S; s++) {
+        cudaStream_t st = g_stage.streams[s];
+        const ss_outputs& so = so_s[s];
+        const int64_t ra = ra_s[s], la = la_s[s], lw = lw_s[s];
+        const int32_t ta = ta_s[s], Ts = Ts_s[s];
 #define D2H(dst, src, bytes) \
     if ((dst) && (bytes) > 0) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st))
-        const size_t nb = (size_t)ns;
+        const size_t nb = (size_t)ns_s[s];
         D2H(ho->req.first_scheduled + ra, so.req.first_scheduled, nb * 8);
         D2H(ho->req.finish_time + ra, so.req.finish_time, nb * 8);
         D2H(ho->req.generated + ra, so.req.generated, nb * 4);
