@@ -28,7 +28,11 @@ struct __align__(16) Dyn {
 };
 
 __device__ __forceinline__ bool klt(const Key& a, const Key& b) {
+#ifdef SS_KLT_SHORT
     return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo);
+#else
+    return (a.hi < b.hi) | ((a.hi == b.hi) & (a.lo < b.lo));  // branch-free (no short-circuit)
+#endif
 }
 __device__ __forceinline__ bool keq(const Key& a, const Key& b) { return a.hi == b.hi && a.lo == b.lo; }
 // branch-free forms for hot warp-synchronous code (no short-circuit branches)
