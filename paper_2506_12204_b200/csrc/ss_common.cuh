@@ -34,7 +34,7 @@ __device__ __forceinline__ bool klt(const Key& a, const Key& b) {
     return (a.hi < b.hi) | ((a.hi == b.hi) & (a.lo < b.lo));  // branch-free (no short-circuit)
 #endif
 }
-__device__ __forceinline__ bool keq(const Key& a, const Key& b) { return a.hi == b.hi && a.lo == b.lo; }
+__device__ __forceinline__ bool keq(const Key& a, const Key& b) { return (a.hi == b.hi) & (a.lo == b.lo); }
 // branch-free forms for hot warp-synchronous code (no short-circuit branches)
 __device__ __forceinline__ bool klt_nb(const Key& a, const Key& b) {
     return (a.hi < b.hi) | ((a.hi == b.hi) & (a.lo < b.lo));

@@ -229,9 +229,10 @@ __device__ __noinline__ int2 q_insert32(const KArgs* Ap, WarpSmem* sm, long long
     // position of each insert in the current FRONT (binary search)
     int lo = 0, hi = T.nF;
     while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (klt(sm->F[mid], key)) lo = mid + 1;
-        else hi = mid;
+        const int mid = (lo + hi) >> 1;
+        const bool below = klt(sm->F[mid], key);  // branch-free step
+        lo = below ? mid + 1 : lo;
+        hi = below ? hi : mid;
     }
     int pos_i = lo + rank_i;
     // FRONT entries shift by the number of inserts below them
@@ -242,8 +243,8 @@ __device__ __noinline__ int2 q_insert32(const KArgs* Ap, WarpSmem* sm, long long
     int s0 = 0, s1 = 0;
     for (int k = 0; k < nI; k++) {
         Key x = sm->X[k];
-        if (h0 && klt(x, e0)) s0++;
-        if (h1 && klt(x, e1)) s1++;
+        s0 += (h0 & klt(x, e0)) ? 1 : 0;
+        s1 += (h1 & klt(x, e1)) ? 1 : 0;
     }
     int p0 = lane + s0, p1 = lane + 32 + s1;
     int total = T.nF + nI;
@@ -1269,18 +1270,20 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     if (c_elig) {
                         int lo = 0, hi = T.nO;
                         while (lo < hi) {
-                            int mid = (lo + hi) >> 1;
-                            if (klt(sm->X[32 + mid], ck)) lo = mid + 1;
-                            else hi = mid;
+                            const int mid = (lo + hi) >> 1;
+                            const bool below = klt(sm->X[32 + mid], ck);  // branch-free step
+                            lo = below ? mid + 1 : lo;
+                            hi = below ? hi : mid;
                         }
                         cnt_c = __popc(cmask & lt) + lo;
                     }
                     if (has_o) {
                         int lo = 0, hi = nc;
                         while (lo < hi) {
-                            int mid = (lo + hi) >> 1;
-                            if (klt(sm->F[mid], okey)) lo = mid + 1;
-                            else hi = mid;
+                            const int mid = (lo + hi) >> 1;
+                            const bool below = klt(sm->F[mid], okey);  // branch-free step
+                            lo = below ? mid + 1 : lo;
+                            hi = below ? hi : mid;
                         }
                         unsigned below = lo >= 32 ? FULL : ((1u << lo) - 1u);
                         cnt_o += __popc(cmask & below);
