@@ -68,6 +68,7 @@ struct HostStage {
     void* hbuf = nullptr;  // pinned host: the slices' rebased offsets
     size_t hcap = 0;
     cudaStream_t streams[SS_MAX_SLICES] = {};
+    int dev = -1;  // device the buffer and streams live on
 };
 constexpr int32_t SLICE_TRACES = SS_SLICE_TRACES;
 HostStage g_stage;
@@ -223,6 +224,19 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
     }
     const size_t total = a16(in_b) + a16(out_b) + a16(log_b) + a16(off_b) + a16(ws_b);
     std::lock_guard<std::mutex> lk(g_stage.mu);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (g_stage.dev != dev && (g_stage.buf || g_stage.streams[0])) {
+        // the staging buffer and streams belong to the device of an earlier call: release them there
+        CK(cudaSetDevice(g_stage.dev));
+        if (g_stage.buf) cudaFree(g_stage.buf);
+        for (auto& st : g_stage.streams)
+            if (st) cudaStreamDestroy(st), st = nullptr;
+        g_stage.buf = nullptr;
+        g_stage.cap = 0;
+        CK(cudaSetDevice(dev));
+    }
+    g_stage.dev = dev;
     if (g_stage.cap < total) {
         if (g_stage.buf) CK(cudaFree(g_stage.buf));
         g_stage.buf = nullptr;
