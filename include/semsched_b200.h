@@ -269,7 +269,12 @@ int ss_run_traces(const ss_params* params, const ss_trace_batch* batch,
 
 /* Same, with every pointer in `batch` and `out` on the HOST (pinned or
  * pageable). Copies in, runs, copies out, synchronises. This is the
- * reference-facing plugin call (host buffers in, host buffers out). */
+ * reference-facing plugin call (host buffers in, host buffers out).
+ * Batches of >= 2,048 traces run as up to 4 slices of consecutive traces on
+ * library-owned streams (which first wait for `stream`): uploads, kernels and
+ * downloads of different slices overlap. Pinned buffers give full overlap.
+ * `kernel_ms` then reports the span from the first slice's prepass to the
+ * last kernel's end. Serialised by a library mutex. */
 int ss_run_traces_host(const ss_params* params, const ss_trace_batch* batch,
                        const ss_outputs* out, void* stream, float* kernel_ms);
 
