@@ -863,6 +863,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     unsigned nmax;            // longest context + 1 (decode step of the batch)
                     long long safe_used;      // no member needs an eviction while used <= this
                     unsigned long long gt;    // this lane's grant term (ss_grant_term of its batch position)
+                    unsigned long long hb;    // chunked kernels: the batch list's hash (sum of the grant terms)
                     // header lanes 29..31: tag pre-multiplied (ss_term); round multiplier of the grant terms
                     const unsigned long long dgc =
                         ((unsigned long long)(lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME)) << 20) * DG;
@@ -880,6 +881,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             safe_used = cap - (long long)maxdem - m;
                         }
                         gt = act ? ss_grant_term((uint32_t)lane, mem.slot) : 0ull;
+                        if (chunking) hb = warp_sum_u64(gt);
                     };
                     // chunked kernels: one call site (one copy of its code) at the loop top;
                     // per-round kernels call it directly (no extra vote per round)
@@ -1126,7 +1128,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                     tr += ss_term(rj, f == 0 ? SS_TAG_HDR : (f == 1 ? SS_TAG_MEM : SS_TAG_TIME), 0, val);
                                 }
                                 // the batch list hashes once: sum of the members' grant terms
-                                const unsigned long long hb = warp_sum_u64(gt);
+                                // hb: the batch list's hash, summed once per membership (setup)
                                 dig += runj ? hb * ss_round_mul(rj) + tr : 0ull;
                             }
                             if (logging) {
