@@ -10,7 +10,10 @@ namespace ss {
 // possible (resident list not kept) / chunked stretches forced by the caller
 constexpr int SS_SEL_PERROUND = 0, SS_SEL_NO_EVICT = 1, SS_SEL_CHUNKED = 2;
 constexpr int FCAP = 64;  // sorted queue-front capacity per trace (shared memory)
-constexpr int WPB = 4;    // traces (warps) per CTA
+#ifndef SS_WPB
+#define SS_WPB 4
+#endif
+constexpr int WPB = SS_WPB;  // traces (warps) per CTA
 
 // Per-request scratch in HBM, indexed like the inputs (trace offset + slot).
 struct Work {
