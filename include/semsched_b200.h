@@ -109,9 +109,18 @@ typedef struct ss_params {
                                   radix sort instead of per-warp queue inserts.
                                   0 = SS_BULK_MIN_DEFAULT, < 0 = never. Results
                                   are identical either way (tests force 1).      */
+    int64_t epilogue_min;      /* grid-wide end of trace: a trace of >= epilogue_min
+                                  requests (config C: one pool of 1M) leaves its
+                                  per-request outputs and waiting-time sums
+                                  (metrics.py:35-56) to two grid-wide kernels
+                                  (exact double-double tile sums, 1e-15 relative to
+                                  CPython's sum) instead of its scheduler warp
+                                  (sequential CPython sum, bit-exact).
+                                  0 = SS_EPILOGUE_MIN_DEFAULT, < 0 = never.      */
 } ss_params;
 
 #define SS_BULK_MIN_DEFAULT 1024
+#define SS_EPILOGUE_MIN_DEFAULT 16384
 
 /* Requests of all traces, concatenated; trace t owns
  * [trace_offsets[t], trace_offsets[t+1]), in pending order. */

@@ -33,6 +33,7 @@ SS_MAX_BATCH = 32
 SS_MAX_LEVELS = 16
 SS_MAX_TRACE_REQS = 1 << 24
 SS_BULK_MIN_DEFAULT = 1024
+SS_EPILOGUE_MIN_DEFAULT = 16384
 
 SS_STAGE_WAITING = 0
 SS_STAGE_DECODING = 2
@@ -54,7 +55,7 @@ class ss_params(C.Structure):
                 ("batch_size", C.c_int32), ("policy", C.c_int32),
                 ("dependency_rule", C.c_int32), ("decode_cost_sum", C.c_int32),
                 ("levels", C.c_int32), ("flags", C.c_uint32), ("max_rounds", C.c_int64),
-                ("bulk_min", C.c_int64)]
+                ("bulk_min", C.c_int64), ("epilogue_min", C.c_int64)]
 
 
 class ss_trace_batch(C.Structure):

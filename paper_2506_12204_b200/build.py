@@ -17,7 +17,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libsemsched_b200.so")
-SOURCES = ["ss_kernel.cu", "ss_prepass.cu", "ss_step.cu", "ss_audit.cu", "ss_api.cu", "ss_tracegen.cpp", "ss_tracegen_dev.cu"]
+SOURCES = ["ss_kernel.cu", "ss_prepass.cu", "ss_epilogue.cu", "ss_step.cu", "ss_audit.cu", "ss_api.cu", "ss_tracegen.cpp", "ss_tracegen_dev.cu"]
 HEADERS = ["ss_kernel.cuh", "ss_common.cuh", "ss_costs.cuh", "../../include/semsched_b200.h",
            "../../include/semsched_tracegen.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -166,6 +166,8 @@ int ss_run_traces(const ss_params* params, const ss_trace_batch* batch, const ss
         cudaError_t e = cudaGetLastError();
         return e != cudaSuccess ? cuda_fail(e, "sched_kernel launch") : fail(rc, "launch failed");
     }
+    rc = ss::launch_epilogue(a, stream);
+    if (rc) return cuda_fail(cudaGetLastError(), "epilogue launch");
     if (kernel_ms) {
         CK(cudaEventRecord(e1, st));
         CK(cudaEventSynchronize(e1));
@@ -357,6 +359,14 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
                 if (k > maxlen) maxlen = k;
             }
             if (maxlen < SS_BULK_MIN_DEFAULT) pp.bulk_min = -1;
+        }
+        if (pp.epilogue_min >= 0) {  // no trace long enough for the grid-wide end: skip its launches
+            int64_t maxlen = 0;
+            for (int32_t t = ta; t < ta + Ts; t++) {
+                const int64_t k = hb->trace_offsets[t + 1] - hb->trace_offsets[t];
+                if (k > maxlen) maxlen = k;
+            }
+            if (maxlen < ss::epilogue_threshold(pp)) pp.epilogue_min = -1;
         }
         const size_t wsz = ss::work_bytes(ns, Ts);
         if (ev_k0 && s == 0) CK(cudaEventRecord(ev_k0, st));

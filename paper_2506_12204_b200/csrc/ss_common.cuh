@@ -46,6 +46,17 @@ __device__ __forceinline__ Key kinf() {
     k.aux = ~0u;
     return k;
 }
+// index t with off[t] <= g < off[t+1] (first such t past empty ranges)
+template <typename I>
+__device__ __forceinline__ int upper_index(const I* off, int n, long long g) {
+    int lo = 0, hi = n;  // search in off[0..n]
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if ((long long)off[mid + 1] <= g) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
 template <int POL>
 __device__ __forceinline__ Key make_key(uint32_t urank, double ft, uint32_t tie, uint32_t slot,
                                         bool decoding) {

@@ -1,0 +1,200 @@
+// ss_epilogue.cu — grid-wide end of trace for long traces.
+//
+// When a trace ends (engine.py:226-243) its per-request records are read out
+// (RequestRecord generated tokens, final f_t / stage) and the waiting-time
+// statistics are reduced (metrics.py:35-56: average wait, per-level and overall
+// normalized wait, over completed records). A short trace does that in its own
+// scheduler warp (ss_kernel.cu, CPython's sequential sum reproduced bit for bit).
+// For a long trace — config C's single pool of 1,000,000 requests — one warp
+// would stream every record alone (26 ms), so traces of >= epilogue_min
+// requests are finished here by the whole grid after the scheduler kernels:
+//
+//   epi_tiles_kernel  one CTA per tile of EPI_TILE requests: coalesced record
+//                     read-out and per-channel double-double partial sums
+//                     (TwoSum, fixed thread order and a fixed shuffle tree:
+//                     deterministic, ~1e-30 relative), one EpiPart per tile;
+//   epi_final_kernel  one warp per long trace: the tiles' partials in a fixed
+//                     order, rounded once to double.
+//
+// The result is the correctly rounded sum except within ~1e-30 of a rounding
+// tie; CPython's Neumaier sum is compensated too, so the two agree to ~1 ulp
+// (tests: 1e-12 relative, north_star's contract is 1e-6).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ss_common.cuh"
+#include "ss_costs.cuh"
+#include "ss_kernel.cuh"
+
+namespace ss {
+
+namespace {
+
+constexpr int EPI_THREADS = 256;
+constexpr int EPI_WARPS = EPI_THREADS / 32;
+
+struct DD {
+    double hi, lo;
+};
+
+// (hi, lo) + b, b a double (TwoSum of the high parts, then renormalise)
+__device__ __forceinline__ DD dd_add1(const DD& a, double b) {
+    const double s = add(a.hi, b);
+    const double bb = sub(s, a.hi);
+    double e = add(sub(a.hi, sub(s, bb)), sub(b, bb));
+    e = add(e, a.lo);
+    DD r;
+    r.hi = add(s, e);
+    r.lo = sub(e, sub(r.hi, s));
+    return r;
+}
+__device__ __forceinline__ DD dd_add(const DD& a, const DD& b) {
+    const double s = add(a.hi, b.hi);
+    const double v = sub(s, a.hi);
+    double e = add(sub(a.hi, sub(s, v)), sub(b.hi, v));
+    e = add(e, add(a.lo, b.lo));
+    DD r;
+    r.hi = add(s, e);
+    r.lo = sub(e, sub(r.hi, s));
+    return r;
+}
+// lane 0 receives the fixed-tree sum of the warp's values
+__device__ __forceinline__ DD dd_warp_sum(DD x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        DD y;
+        y.hi = __shfl_down_sync(FULL, x.hi, o);
+        y.lo = __shfl_down_sync(FULL, x.lo, o);
+        x = dd_add(x, y);
+    }
+    return x;
+}
+
+__global__ void __launch_bounds__(EPI_THREADS) epi_tiles_kernel(const __grid_constant__ KArgs A) {
+    const int T = A.in.n_traces;
+    const long long E = A.w.epoff[T];
+    if (E == 0) return;
+    __shared__ DD red[EPI_WARPS][EPI_CH];
+    __shared__ int rcnt[EPI_WARPS][SS_MAX_LEVELS + 1];
+    const Dyn* DY = reinterpret_cast<const Dyn*>(A.w.dy);
+    EpiPart* PT = reinterpret_cast<EpiPart*>(A.w.epart);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (long long e = blockIdx.x; e < E; e += gridDim.x) {
+        const int t = upper_index(A.w.epoff, T, e);
+        const long long j = e - A.w.epoff[t];
+        const long long off = A.in.trace_offsets[t], n = A.in.trace_offsets[t + 1] - off;
+        const long long i0 = j * EPI_TILE, i1 = (i0 + EPI_TILE < n) ? i0 + EPI_TILE : n;
+        DD acc[EPI_CH];
+        int cnt[SS_MAX_LEVELS + 1];
+#pragma unroll
+        for (int c = 0; c < EPI_CH; c++) acc[c].hi = acc[c].lo = 0.0;
+#pragma unroll
+        for (int c = 0; c <= SS_MAX_LEVELS; c++) cnt[c] = 0;
+        for (long long i = i0 + threadIdx.x; i < i1; i += EPI_THREADS) {
+            // RequestRecord read-out, as the scheduler warp does for short traces
+            const long long g = off + i;
+            const Dyn d = DY[g];
+            A.out.req.generated[g] = d.dec;
+            if (A.out.req.f_t) A.out.req.f_t[g] = d.ft;
+            if (A.out.req.state) A.out.req.state[g] = (d.flg & F_STAGE) | ((d.flg & F_PF) ? 256u : 0u);
+            const double fi = A.out.req.finish_time[g];
+            if (!isnan(fi)) {  // completed (metrics.py:24-32)
+                const double w = sub(fi, A.in.arrival_time[g]);
+                const double nw = dv(w, (double)d.dec);
+                const int lv = A.in.true_urgency[g];
+                acc[EPI_CH - 1] = dd_add1(acc[EPI_CH - 1], w);
+                acc[EPI_CH - 2] = dd_add1(acc[EPI_CH - 2], nw);
+#pragma unroll
+                for (int l = 0; l < SS_MAX_LEVELS; l++) {
+                    if (lv == l) {
+                        acc[l] = dd_add1(acc[l], nw);
+                        cnt[l] += 1;
+                    }
+                }
+                cnt[SS_MAX_LEVELS] += 1;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < EPI_CH; c++) {
+            const DD x = dd_warp_sum(acc[c]);
+            if (lane == 0) red[wid][c] = x;
+        }
+#pragma unroll
+        for (int c = 0; c <= SS_MAX_LEVELS; c++) {
+            const int s = __reduce_add_sync(FULL, cnt[c]);
+            if (lane == 0) rcnt[wid][c] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x < EPI_CH) {
+            DD x = red[0][threadIdx.x];
+            for (int w = 1; w < EPI_WARPS; w++) x = dd_add(x, red[w][threadIdx.x]);
+            PT[e].hi[threadIdx.x] = x.hi;
+            PT[e].lo[threadIdx.x] = x.lo;
+        }
+        if (threadIdx.x <= SS_MAX_LEVELS) {
+            int s = 0;
+            for (int w = 0; w < EPI_WARPS; w++) s += rcnt[w][threadIdx.x];
+            PT[e].cnt[threadIdx.x] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// one warp per long trace: its tiles' partials, fixed order, one rounding
+__global__ void __launch_bounds__(EPI_THREADS) epi_final_kernel(const __grid_constant__ KArgs A) {
+    const int T = A.in.n_traces;
+    if (A.w.epoff[T] == 0) return;
+    const int t = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= T) return;
+    const int k = A.w.epT[t];
+    if (k == 0) return;
+    const EpiPart* PT = reinterpret_cast<const EpiPart*>(A.w.epart) + A.w.epoff[t];
+    ss_trace_stats* st = A.out.stats + t;
+    for (int c = 0; c < EPI_CH; c++) {
+        DD x;
+        x.hi = x.lo = 0.0;
+        for (int i = lane; i < k; i += 32) {
+            DD y;
+            y.hi = PT[i].hi[c];
+            y.lo = PT[i].lo[c];
+            x = dd_add(x, y);
+        }
+        x = dd_warp_sum(x);
+        if (lane == 0) {
+            const double v = add(x.hi, x.lo);
+            if (c < SS_MAX_LEVELS) st->level_norm_sum[c] = v;
+            else if (c == SS_MAX_LEVELS) st->sum_norm_wait = v;
+            else st->sum_wait = v;
+        }
+    }
+    for (int c = 0; c <= SS_MAX_LEVELS; c++) {
+        int s = 0;
+        for (int i = lane; i < k; i += 32) s += PT[i].cnt[c];
+        s = __reduce_add_sync(FULL, s);
+        if (lane == 0) {
+            if (c < SS_MAX_LEVELS) st->level_count[c] = s;
+            else st->completed = s;
+        }
+    }
+}
+
+}  // namespace
+
+int launch_epilogue(const KArgs& a, void* stream) {
+    if (epilogue_threshold(a.P) <= 0 || a.in.n_traces == 0 || a.in.n_requests == 0) return SS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // tiles in a grid-stride loop (the tile count lives on the device)
+    const long long tiles_bound = a.in.n_requests / EPI_TILE + a.in.n_traces + 1;
+    const int grid = (int)(tiles_bound < 2LL * sms ? tiles_bound : 2LL * sms);
+    epi_tiles_kernel<<<grid, EPI_THREADS, 0, st>>>(a);
+    const long long warps = a.in.n_traces;
+    epi_final_kernel<<<(int)((warps * 32 + EPI_THREADS - 1) / EPI_THREADS), EPI_THREADS, 0, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? SS_OK : SS_ERR_CUDA;
+}
+
+}  // namespace ss

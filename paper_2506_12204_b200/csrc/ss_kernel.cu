@@ -1877,12 +1877,15 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             T.nins = 0;
         }
 
-        // ---- outputs and the fused statistics (metrics.py:35-56)
+        // ---- outputs and the fused statistics (metrics.py:35-56); a long trace
+        // (config C's 1M pool) leaves both to the grid-wide epilogue (ss_epilogue.cu)
         SS_SECT(4);
         {
+            const long long epi_min = epilogue_threshold(A.P);
+            const bool warp_end = !(epi_min > 0 && (long long)n >= epi_min);
             PySum acc;
             acc.init();
-            for (int base = 0; uni(base < n); base += 32) {
+            for (int base = 0; uni(warp_end && base < n); base += 32) {
                 const int i = base + lane;
                 double w = 0.0, nw = 0.0;
                 bool fin = false;
@@ -1917,14 +1920,16 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             const int cntv = acc.n;
             __syncwarp();
             ss_trace_stats* st = A.out.stats + t;
-            if (lane < SS_MAX_LEVELS) {
-                st->level_norm_sum[lane] = val;
-                st->level_count[lane] = cntv;
-            }
-            if (lane == 30) st->sum_norm_wait = val;
-            if (lane == 31) {
-                st->sum_wait = val;
-                st->completed = cntv;
+            if (warp_end) {
+                if (lane < SS_MAX_LEVELS) {
+                    st->level_norm_sum[lane] = val;
+                    st->level_count[lane] = cntv;
+                }
+                if (lane == 30) st->sum_norm_wait = val;
+                if (lane == 31) {
+                    st->sum_wait = val;
+                    st->completed = cntv;
+                }
             }
             if (lane == 0) {
                 st->digest = want_digest ? dig : 0ull;
@@ -1963,6 +1968,10 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
 static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 static long long tiles_for(int64_t n) { return ((n > 0 ? n : 1) + RS_TILE - 1) / RS_TILE; }
+// every trace has ceil(n_t / EPI_TILE) <= n_t / EPI_TILE + 1 epilogue tiles
+static size_t epi_tiles_max(int64_t n, int32_t T) {
+    return (size_t)(n > 0 ? n : 1) / EPI_TILE + (size_t)(T > 0 ? T : 1) + 1;
+}
 
 // Layout: zero-initialised block first (one memset per run), then scratch.
 size_t work_bytes(int64_t n, int32_t T) {
@@ -1970,7 +1979,8 @@ size_t work_bytes(int64_t n, int32_t T) {
     size_t zero = 2 * align16(tt * 8) + align16(tt * 4) + align16((size_t)RS_PASSES * 256 * 4) + 16;
     // st, dy, B, ins, S, k0: 16 B; rpos, R, pend, tt0, tt1: 4 B
     return zero + 6 * align16(nn * 16) + 5 * align16(nn * 4) + align16(tt * 4) + align16((tt + 1) * 8) +
-           align16((size_t)(RS_PASSES + 1) * 4) + align16((size_t)256 * tiles_for(n) * 4);
+           align16((size_t)(RS_PASSES + 1) * 4) + align16((size_t)256 * tiles_for(n) * 4) +
+           align16(tt * 4) + align16((tt + 1) * 8) + align16(epi_tiles_max(n, T) * sizeof(EpiPart));
 }
 
 size_t work_zero_bytes(int32_t T) {
@@ -2000,8 +2010,11 @@ void carve_work(void* base, int64_t n, int32_t T, Work* w) {
     w->bulkP = (int*)p;      p += align16(tt * 4);
     w->eoff = (long long*)p; p += align16((tt + 1) * 8);
     w->plan = (int*)p;       p += align16((size_t)(RS_PASSES + 1) * 4);
-    w->tcnt = (uint32_t*)p;
+    w->tcnt = (uint32_t*)p;  p += align16((size_t)256 * tiles_for(n) * 4);
     w->tiles_max = tiles_for(n);
+    w->epT = (int*)p;        p += align16(tt * 4);
+    w->epoff = (long long*)p; p += align16((tt + 1) * 8);
+    w->epart = (void*)p;
 }
 
 int sched_smem_bytes() { return (int)(sizeof(WarpSmem) * WPB); }

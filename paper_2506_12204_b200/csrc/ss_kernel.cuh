@@ -39,6 +39,10 @@ struct Work {
     int* plan;                // [RS_PASSES] source buffer of each pass (-1: skipped), [RS_PASSES]: final
     uint32_t* tcnt;           // [256][tiles] per-tile digit counts -> scanned offsets
     long long tiles_max;      // capacity of tcnt in tiles
+    // ---- grid-wide end of trace (ss_epilogue.cu) ----------------------------
+    int* epT;                 // per trace: epilogue tiles (0: the scheduler warp finishes the trace)
+    long long* epoff;         // per trace + 1: exclusive scan of epT
+    void* epart;              // per epilogue tile: partial sums (EpiPart)
     int* next_trace;     // work counter for persistent warps
 };
 
@@ -53,6 +57,20 @@ constexpr int PP_THREADS = 256;               // prepass CTA size
 constexpr int RS_ITEMS = 16;                  // radix sort: keys per thread per tile
 constexpr int RS_TILE = PP_THREADS * RS_ITEMS;
 constexpr int RS_PASSES = 16;                 // 8-bit digits: lo 4, hi 8, trace index 4
+constexpr int EPI_TILE = 4096;                // requests per epilogue tile (one CTA)
+constexpr int EPI_CH = SS_MAX_LEVELS + 2;     // sums: level 0..15, normalized wait, wait
+
+// per-tile partial sums of the grid-wide epilogue: double-double per channel
+struct __align__(16) EpiPart {
+    double hi[EPI_CH], lo[EPI_CH];
+    int cnt[SS_MAX_LEVELS + 1];  // per level, completed
+    int _pad[3];
+};
+
+// traces of >= this many requests finish in the grid-wide epilogue (0 = never)
+__host__ __device__ __forceinline__ long long epilogue_threshold(const ss_params& P) {
+    return P.epilogue_min == 0 ? (long long)SS_EPILOGUE_MIN_DEFAULT : (P.epilogue_min < 0 ? 0 : P.epilogue_min);
+}
 
 size_t work_bytes(int64_t n_requests, int32_t n_traces);
 void carve_work(void* base, int64_t n_requests, int32_t n_traces, Work* w);
@@ -60,6 +78,8 @@ size_t work_zero_bytes(int32_t n_traces);  // leading bytes of the workspace zer
 // grid-wide prepass: request init, per-trace tallies, bulk-admission sort
 int launch_prepass(const KArgs& a, void* stream);
 int launch_sched(const KArgs& a, int blocks, void* stream);
+// grid-wide end of trace for long traces (per-request outputs + statistics)
+int launch_epilogue(const KArgs& a, void* stream);
 int sched_launches(int policy);  // scheduler kernel launches per run
 int sched_smem_bytes();
 int sched_max_blocks(int policy, int* sm_count);

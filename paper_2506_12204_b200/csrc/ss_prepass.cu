@@ -38,18 +38,6 @@ __device__ __forceinline__ unsigned lanemask_lt_pp() {
     return r;
 }
 
-// index t with off[t] <= g < off[t+1] (first such t past empty ranges)
-template <typename I>
-__device__ __forceinline__ int upper_index(const I* off, int n, long long g) {
-    int lo = 0, hi = n;  // search in off[0..n]
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if ((long long)off[mid + 1] <= g) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
 __device__ __forceinline__ long long bulk_threshold(const ss_params& P) {
     return P.bulk_min == 0 ? (long long)SS_BULK_MIN_DEFAULT : P.bulk_min;
 }
@@ -82,19 +70,21 @@ __global__ void detect_kernel(const __grid_constant__ KArgs A) {
         }
     }
     A.w.bulkP[t] = P;
+    // grid-wide end of trace (ss_epilogue.cu) for long traces
+    const long long em = epilogue_threshold(A.P);
+    A.w.epT[t] = (em > 0 && n >= em) ? (int)((n + EPI_TILE - 1) / EPI_TILE) : 0;
 }
 
-// exclusive scan of bulkP -> eoff (single CTA, chunked)
-__global__ void __launch_bounds__(1024) eoff_scan_kernel(const __grid_constant__ KArgs A) {
+// exclusive scan of in[0..T) -> out[0..T] (single CTA, chunked)
+__device__ void block_scan(const int* in, long long* out, int T) {
     __shared__ long long wsum[32];
     __shared__ long long carry;
-    const int T = A.in.n_traces;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     for (int base = 0; base < T; base += 1024) {
         const int t = base + threadIdx.x;
-        long long v = t < T ? (long long)A.w.bulkP[t] : 0;
+        long long v = t < T ? (long long)in[t] : 0;
         long long x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -114,12 +104,19 @@ __global__ void __launch_bounds__(1024) eoff_scan_kernel(const __grid_constant__
         }
         __syncthreads();
         const long long pre = carry + (wid ? wsum[wid - 1] : 0) + x - v;
-        if (t < T) A.w.eoff[t] = pre;
+        if (t < T) out[t] = pre;
         __syncthreads();
         if (threadIdx.x == 1023) carry = pre + v;
         __syncthreads();
     }
-    if (threadIdx.x == 0) A.w.eoff[T] = carry;
+    if (threadIdx.x == 0) out[T] = carry;
+    __syncthreads();
+}
+
+// bulkP -> eoff (bulk runs), epT -> epoff (epilogue tiles)
+__global__ void __launch_bounds__(1024) eoff_scan_kernel(const __grid_constant__ KArgs A) {
+    block_scan(A.w.bulkP, A.w.eoff, A.in.n_traces);
+    block_scan(A.w.epT, A.w.epoff, A.in.n_traces);
 }
 
 // ---- 2. request init: one thread per request --------------------------------

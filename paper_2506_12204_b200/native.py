@@ -76,7 +76,18 @@ def launches_per_run(params=None, max_trace_len=None) -> int:
     # launch the three variants (chunked without eviction, chunked, per-round); the
     # unselected ones exit at once
     sched = 3 if params is None or params.policy == A.SS_POLICY["semantic"] else 1
-    return 4 + (3 + 16 * 3 + 1 if bulk else 0) + sched
+    epi = 2 if params is None or _epilogue_possible(params, max_trace_len) else 0
+    return 4 + (3 + 16 * 3 + 1 if bulk else 0) + sched + epi
+
+
+def _epilogue_threshold(params) -> int:
+    return A.SS_EPILOGUE_MIN_DEFAULT if params.epilogue_min == 0 else max(int(params.epilogue_min), 0)
+
+
+def _epilogue_possible(params, max_trace_len=None) -> bool:
+    """Whether any trace is long enough for the grid-wide end of trace."""
+    thr = _epilogue_threshold(params)
+    return thr > 0 and (max_trace_len is None or max_trace_len >= thr)
 
 
 def _bulk_possible(params, max_trace_len: int) -> bool:
@@ -88,13 +99,21 @@ def _bulk_possible(params, max_trace_len: int) -> bool:
 
 
 def _with_bulk(params, max_trace_len):
-    """A copy of params with the bulk-sort stage disabled when no trace is long
-    enough to need it (saves its 52 empty launches; results are identical)."""
-    if max_trace_len is None or _bulk_possible(params, max_trace_len) or params.bulk_min < 0:
+    """A copy of params with the bulk-sort stage and the grid-wide end of trace
+    disabled when no trace is long enough to need them (saves their empty
+    launches; results are identical)."""
+    if max_trace_len is None:
+        return params
+    no_bulk = not _bulk_possible(params, max_trace_len) and params.bulk_min >= 0
+    no_epi = not _epilogue_possible(params, max_trace_len) and params.epilogue_min >= 0
+    if not (no_bulk or no_epi):
         return params
     q = A.ss_params()
     C.pointer(q)[0] = params
-    q.bulk_min = -1
+    if no_bulk:
+        q.bulk_min = -1
+    if no_epi:
+        q.epilogue_min = -1
     return q
 
 

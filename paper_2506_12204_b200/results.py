@@ -18,7 +18,8 @@ from . import _abi as A
 
 def make_params(profile, batch_size: int, memory_capacity: int, policy: str = "semantic",
                 dependency_rule: bool = True, decode_batch_cost: str = "max", levels: int = 5,
-                flags: int = A.SS_FLAG_DIGEST, max_rounds: int = 0, bulk_min: int = 0) -> A.ss_params:
+                flags: int = A.SS_FLAG_DIGEST, max_rounds: int = 0, bulk_min: int = 0,
+                epilogue_min: int = 0) -> A.ss_params:
     """``profile`` is any object with alpha1..beta_save attributes or a dict."""
     g = (lambda k: profile[k]) if isinstance(profile, dict) else (lambda k: getattr(profile, k))
     if decode_batch_cost not in ("max", "sum"):
@@ -39,6 +40,7 @@ def make_params(profile, batch_size: int, memory_capacity: int, policy: str = "s
     p.flags = int(flags)
     p.max_rounds = int(max_rounds)
     p.bulk_min = int(bulk_min)
+    p.epilogue_min = int(epilogue_min)
     return p
 
 

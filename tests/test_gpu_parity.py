@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from conftest import case_batch, case_params, golden_cases
-from parity_helpers import check_against_golden
+from parity_helpers import check_against_golden, compare_with_oracle as _compare_with_oracle
 from paper_2506_12204_b200 import _abi as A
 
 pytestmark = pytest.mark.gpu
@@ -68,34 +68,6 @@ def _seeded_batch(n_traces, total, cfg_kw=None, seed0=0):
         cfg = ScenarioConfig(workload=WorkloadSpec(total_requests=total, seed=s, **(cfg_kw or {})), seed=s)
         parts.append(prepare_trace(generate(cfg.workload), cfg)[0])
     return TraceBatch.concat(parts), cfg
-
-
-def _compare_with_oracle(gpu, cpu, batch):
-    """Statuses must agree everywhere; every other field is compared on the
-    traces both finished (a reference exception ends a trace mid-round)."""
-    assert np.array_equal(gpu.stats["status"], cpu.stats["status"]), "status"
-    # a reference exception ends the trace at an observable round (the raising
-    # round counts on both sides); a trace the reference would never finish
-    # (livelock / round cap) has no observable round count (DESIGN.md §5)
-    obs = (cpu.stats["status"] == 0) | (cpu.stats["status"] == A.SS_TRACE_REF_ERROR)
-    assert np.array_equal(gpu.stats["rounds"][obs], cpu.stats["rounds"][obs]), "rounds (incl. reference errors)"
-    ok = cpu.stats["status"] == 0
-    for k in ("rounds", "evictions", "digest", "completed", "unservable", "mem_used_peak",
-              "lost_evictions", "anomalies", "sum_pool", "sum_granted", "sum_victims",
-              "sum_resident_evict"):
-        assert np.array_equal(gpu.stats[k][ok], cpu.stats[k][ok]), k
-    for k in ("final_clock", "sum_wait", "sum_norm_wait", "level_norm_sum"):
-        assert np.array_equal(gpu.stats[k][ok].view(np.uint64), cpu.stats[k][ok].view(np.uint64)), k
-    assert np.array_equal(gpu.stats["level_count"][ok], cpu.stats["level_count"][ok])
-    sizes = np.diff(batch.offsets)
-    rmask = np.repeat(ok, sizes)
-    for k in ("first_scheduled", "finish_time", "f_t"):
-        assert np.array_equal(getattr(gpu, k)[rmask].view(np.uint64), getattr(cpu, k)[rmask].view(np.uint64)), k
-    for k in ("generated", "evictions"):
-        assert np.array_equal(getattr(gpu, k)[rmask], getattr(cpu, k)[rmask]), k
-    for t in np.nonzero(ok)[0]:
-        assert np.array_equal(gpu.unservable[t], cpu.unservable[t])
-    return int(ok.sum())
 
 
 @pytest.mark.parametrize("capacity", [10**9, 1500, 700])
