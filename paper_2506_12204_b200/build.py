@@ -47,8 +47,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     objdir = LIBDIR if out is None else tempfile.mkdtemp(prefix="ss_build_")  # variants build in parallel
-    objs = []
-    for src in SOURCES:
+    def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         if src.endswith(".cpp"):
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread",
@@ -57,7 +56,12 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
             cmd = ([nvcc()] + NVCC_FLAGS + ["-Xptxas", "-v"] * verbose + [f"-D{d}" for d in defines]
                    + ["-c", os.path.join(CSRC, src), "-o", obj])
         subprocess.run(cmd, check=True)
-        objs.append(obj)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = lib + ".tmp"
     subprocess.run([nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs, check=True)
     os.replace(tmp, lib)

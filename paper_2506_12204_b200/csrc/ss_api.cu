@@ -198,6 +198,18 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
         return SS_OK;
     }
     const bool logr = (params->flags & SS_FLAG_ROUND_LOG) != 0;
+    // host offsets: the copies below read [offsets[t], offsets[t+1]) of every array
+    if (hb->trace_offsets[0] != 0 || hb->trace_offsets[T] != n)
+        return fail(SS_ERR_INVALID_ARG, "trace_offsets must start at 0 and end at n_requests");
+    for (int32_t t = 0; t < T; t++)
+        if (hb->trace_offsets[t + 1] < hb->trace_offsets[t])
+            return fail(SS_ERR_INVALID_ARG, "trace_offsets must be nondecreasing");
+    if (logr) {
+        if (ho->log_offsets[0] != 0) return fail(SS_ERR_INVALID_ARG, "log_offsets must start at 0");
+        for (int32_t t = 0; t < T; t++)
+            if (ho->log_offsets[t + 1] < ho->log_offsets[t])
+                return fail(SS_ERR_INVALID_ARG, "log_offsets must be nondecreasing");
+    }
     // Slices of consecutive traces, each on its own stream: slice s+1's inputs
     // upload while slice s computes, slice s's outputs download while later
     // slices compute, and a later slice's CTAs fill the SM slots an earlier
@@ -290,135 +302,152 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
     // the slices start after the caller's stream work
     cudaStream_t cs = (cudaStream_t)stream;
     cudaEvent_t ev_in = nullptr, ev_k0 = nullptr, ev_k1[SS_MAX_SLICES] = {};
-    CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
-    CK(cudaEventRecord(ev_in, cs));
-    if (kernel_ms && S > 1) {
-        CK(cudaEventCreate(&ev_k0));
-        for (int s = 0; s < S; s++) CK(cudaEventCreate(&ev_k1[s]));
-    }
-    size_t ooff = 0, wsoff = 0;
-    ss_outputs so_s[SS_MAX_SLICES];
-    int64_t ra_s[SS_MAX_SLICES], ns_s[SS_MAX_SLICES], la_s[SS_MAX_SLICES], lw_s[SS_MAX_SLICES];
-    int32_t ta_s[SS_MAX_SLICES], Ts_s[SS_MAX_SLICES];
-    for (int s = 0; s < S; s++) {
-        cudaStream_t st = g_stage.streams[s];
-        CK(cudaStreamWaitEvent(st, ev_in, 0));
-        const int32_t ta = t0s[s], Ts = t0s[s + 1] - t0s[s];
-        const int64_t ra = hb->trace_offsets[ta], ns = hb->trace_offsets[t0s[s + 1]] - ra;
-        // rebased trace (and log) offsets of this slice
-        int64_t* ho_off = (int64_t*)(h_offs + ooff);
-        int64_t* do_off = (int64_t*)(d_offs + ooff);
-        for (int32_t t = 0; t <= Ts; t++) ho_off[t] = hb->trace_offsets[ta + t] - ra;
-        CK(cudaMemcpyAsync(do_off, ho_off, (size_t)(Ts + 1) * 8, cudaMemcpyHostToDevice, st));
-        ooff += a16((size_t)(Ts + 1) * 8);
-        ss_trace_batch sb = db;
-        sb.n_traces = Ts;
-        sb.n_requests = ns;
-        sb.trace_offsets = do_off;
-#define H2D(field, esz)                                                                                  \
-    do {                                                                                                 \
-        sb.field = db.field + ra;                                                                        \
-        if (ns > 0) CK(cudaMemcpyAsync((void*)sb.field, hb->field + ra, (size_t)ns * (esz), cudaMemcpyHostToDevice, st)); \
-    } while (0)
-        H2D(ready_time, 8);
-        H2D(arrival_time, 8);
-        H2D(prompt_len, 4);
-        H2D(true_output_len, 4);
-        H2D(pred_len, 4);
-        H2D(pred_urgency, 1);
-        H2D(true_urgency, 1);
-        H2D(tie_rank, 4);
-#undef H2D
-        ss_outputs so = dout;
-        so.req.first_scheduled += ra;
-        so.req.finish_time += ra;
-        so.req.generated += ra;
-        so.req.evictions += ra;
-        if (so.req.f_t) so.req.f_t += ra;
-        if (so.req.state) so.req.state += ra;
-        so.stats += ta;
-        so.unservable_slots += ra;
-        int64_t la = 0, lw = 0;
-        if (logr) {
-            la = ho->log_offsets[ta];
-            lw = ho->log_offsets[t0s[s + 1]] - la;
-            int64_t* hl = (int64_t*)(h_offs + ooff);
-            int64_t* dl = (int64_t*)(d_offs + ooff);
-            for (int32_t t = 0; t <= Ts; t++) hl[t] = ho->log_offsets[ta + t] - la;
-            CK(cudaMemcpyAsync(dl, hl, (size_t)(Ts + 1) * 8, cudaMemcpyHostToDevice, st));
+    auto drop_events = [&]() {
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (ev_k0) cudaEventDestroy(ev_k0);
+        for (auto& e : ev_k1)
+            if (e) cudaEventDestroy(e), e = nullptr;
+        ev_in = ev_k0 = nullptr;
+    };
+    // every slice's uploads, kernels and downloads; an error return leaves
+    // work queued on the slice streams, which must drain before the staging
+    // buffers (and the g_stage lock) are given up
+    auto run_slices = [&]() -> int {
+        CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev_in, cs));
+        if (kernel_ms && S > 1) {
+            CK(cudaEventCreate(&ev_k0));
+            for (int s = 0; s < S; s++) CK(cudaEventCreate(&ev_k1[s]));
+        }
+        size_t ooff = 0, wsoff = 0;
+        ss_outputs so_s[SS_MAX_SLICES];
+        int64_t ra_s[SS_MAX_SLICES], ns_s[SS_MAX_SLICES], la_s[SS_MAX_SLICES], lw_s[SS_MAX_SLICES];
+        int32_t ta_s[SS_MAX_SLICES], Ts_s[SS_MAX_SLICES];
+        for (int s = 0; s < S; s++) {
+            cudaStream_t st = g_stage.streams[s];
+            CK(cudaStreamWaitEvent(st, ev_in, 0));
+            const int32_t ta = t0s[s], Ts = t0s[s + 1] - t0s[s];
+            const int64_t ra = hb->trace_offsets[ta], ns = hb->trace_offsets[t0s[s + 1]] - ra;
+            // rebased trace (and log) offsets of this slice
+            int64_t* ho_off = (int64_t*)(h_offs + ooff);
+            int64_t* do_off = (int64_t*)(d_offs + ooff);
+            for (int32_t t = 0; t <= Ts; t++) ho_off[t] = hb->trace_offsets[ta + t] - ra;
+            CK(cudaMemcpyAsync(do_off, ho_off, (size_t)(Ts + 1) * 8, cudaMemcpyHostToDevice, st));
             ooff += a16((size_t)(Ts + 1) * 8);
-            so.round_log += la;
-            so.log_offsets = dl;
-        }
-        // no trace of the slice long enough for a bulk first round: skip the bulk-sort stage
-        ss_params pp = *params;
-        if (pp.bulk_min == 0) {
-            int64_t maxlen = 0;
-            for (int32_t t = ta; t < ta + Ts; t++) {
-                const int64_t k = hb->trace_offsets[t + 1] - hb->trace_offsets[t];
-                if (k > maxlen) maxlen = k;
+            ss_trace_batch sb = db;
+            sb.n_traces = Ts;
+            sb.n_requests = ns;
+            sb.trace_offsets = do_off;
+#define H2D(field, esz)                                                                                  \
+        do {                                                                                                 \
+            sb.field = db.field + ra;                                                                        \
+            if (ns > 0) CK(cudaMemcpyAsync((void*)sb.field, hb->field + ra, (size_t)ns * (esz), cudaMemcpyHostToDevice, st)); \
+        } while (0)
+            H2D(ready_time, 8);
+            H2D(arrival_time, 8);
+            H2D(prompt_len, 4);
+            H2D(true_output_len, 4);
+            H2D(pred_len, 4);
+            H2D(pred_urgency, 1);
+            H2D(true_urgency, 1);
+            H2D(tie_rank, 4);
+#undef H2D
+            ss_outputs so = dout;
+            so.req.first_scheduled += ra;
+            so.req.finish_time += ra;
+            so.req.generated += ra;
+            so.req.evictions += ra;
+            if (so.req.f_t) so.req.f_t += ra;
+            if (so.req.state) so.req.state += ra;
+            so.stats += ta;
+            so.unservable_slots += ra;
+            int64_t la = 0, lw = 0;
+            if (logr) {
+                la = ho->log_offsets[ta];
+                lw = ho->log_offsets[t0s[s + 1]] - la;
+                int64_t* hl = (int64_t*)(h_offs + ooff);
+                int64_t* dl = (int64_t*)(d_offs + ooff);
+                for (int32_t t = 0; t <= Ts; t++) hl[t] = ho->log_offsets[ta + t] - la;
+                CK(cudaMemcpyAsync(dl, hl, (size_t)(Ts + 1) * 8, cudaMemcpyHostToDevice, st));
+                ooff += a16((size_t)(Ts + 1) * 8);
+                so.round_log += la;
+                so.log_offsets = dl;
             }
-            if (maxlen < SS_BULK_MIN_DEFAULT) pp.bulk_min = -1;
-        }
-        if (pp.epilogue_min >= 0) {  // no trace long enough for the grid-wide end: skip its launches
-            int64_t maxlen = 0;
-            for (int32_t t = ta; t < ta + Ts; t++) {
-                const int64_t k = hb->trace_offsets[t + 1] - hb->trace_offsets[t];
-                if (k > maxlen) maxlen = k;
+            // no trace of the slice long enough for a bulk first round: skip the bulk-sort stage
+            ss_params pp = *params;
+            if (pp.bulk_min == 0) {
+                int64_t maxlen = 0;
+                for (int32_t t = ta; t < ta + Ts; t++) {
+                    const int64_t k = hb->trace_offsets[t + 1] - hb->trace_offsets[t];
+                    if (k > maxlen) maxlen = k;
+                }
+                if (maxlen < SS_BULK_MIN_DEFAULT) pp.bulk_min = -1;
             }
-            if (maxlen < ss::epilogue_threshold(pp)) pp.epilogue_min = -1;
+            if (pp.epilogue_min >= 0) {  // no trace long enough for the grid-wide end: skip its launches
+                int64_t maxlen = 0;
+                for (int32_t t = ta; t < ta + Ts; t++) {
+                    const int64_t k = hb->trace_offsets[t + 1] - hb->trace_offsets[t];
+                    if (k > maxlen) maxlen = k;
+                }
+                if (maxlen < ss::epilogue_threshold(pp)) pp.epilogue_min = -1;
+            }
+            const size_t wsz = ss::work_bytes(ns, Ts);
+            if (ev_k0 && s == 0) CK(cudaEventRecord(ev_k0, st));
+            // one slice: the call times its prepass and kernel itself (ss_last_timings)
+            rc = ss_run_traces(&pp, &sb, &so, d_ws + wsoff, wsz, (void*)st, S == 1 ? kernel_ms : nullptr);
+            if (rc) return rc;
+            wsoff += a16(wsz);
+            if (ev_k0) CK(cudaEventRecord(ev_k1[s], st));
+            so_s[s] = so;
+            ra_s[s] = ra;
+            ns_s[s] = ns;
+            ta_s[s] = ta;
+            Ts_s[s] = Ts;
+            la_s[s] = la;
+            lw_s[s] = lw;
         }
-        const size_t wsz = ss::work_bytes(ns, Ts);
-        if (ev_k0 && s == 0) CK(cudaEventRecord(ev_k0, st));
-        // one slice: the call times its prepass and kernel itself (ss_last_timings)
-        rc = ss_run_traces(&pp, &sb, &so, d_ws + wsoff, wsz, (void*)st, S == 1 ? kernel_ms : nullptr);
-        if (rc) return rc;
-        wsoff += a16(wsz);
-        if (ev_k0) CK(cudaEventRecord(ev_k1[s], st));
-        so_s[s] = so;
-        ra_s[s] = ra;
-        ns_s[s] = ns;
-        ta_s[s] = ta;
-        Ts_s[s] = Ts;
-        la_s[s] = la;
-        lw_s[s] = lw;
-    }
-    // downloads only after every slice's work is queued: a pageable destination makes
-    // cudaMemcpyAsync block the host, which must not delay the later slices' uploads
-    for (int s = 0; s < S; s++) {
-        cudaStream_t st = g_stage.streams[s];
-        const ss_outputs& so = so_s[s];
-        const int64_t ra = ra_s[s], la = la_s[s], lw = lw_s[s];
-        const int32_t ta = ta_s[s], Ts = Ts_s[s];
+        // downloads only after every slice's work is queued: a pageable destination makes
+        // cudaMemcpyAsync block the host, which must not delay the later slices' uploads
+        for (int s = 0; s < S; s++) {
+            cudaStream_t st = g_stage.streams[s];
+            const ss_outputs& so = so_s[s];
+            const int64_t ra = ra_s[s], la = la_s[s], lw = lw_s[s];
+            const int32_t ta = ta_s[s], Ts = Ts_s[s];
 #define D2H(dst, src, bytes) \
-    if ((dst) && (bytes) > 0) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st))
-        const size_t nb = (size_t)ns_s[s];
-        D2H(ho->req.first_scheduled + ra, so.req.first_scheduled, nb * 8);
-        D2H(ho->req.finish_time + ra, so.req.finish_time, nb * 8);
-        D2H(ho->req.generated + ra, so.req.generated, nb * 4);
-        D2H(ho->req.evictions + ra, so.req.evictions, nb * 4);
-        if (ho->req.f_t) D2H(ho->req.f_t + ra, so.req.f_t, nb * 8);
-        if (ho->req.state) D2H(ho->req.state + ra, so.req.state, nb * 4);
-        D2H(ho->stats + ta, so.stats, (size_t)Ts * sizeof(ss_trace_stats));
-        D2H(ho->unservable_slots + ra, so.unservable_slots, nb * 4);
-        if (logr) D2H(ho->round_log + la, so.round_log, (size_t)lw * 4);
+        if ((dst) && (bytes) > 0) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st))
+            const size_t nb = (size_t)ns_s[s];
+            D2H(ho->req.first_scheduled + ra, so.req.first_scheduled, nb * 8);
+            D2H(ho->req.finish_time + ra, so.req.finish_time, nb * 8);
+            D2H(ho->req.generated + ra, so.req.generated, nb * 4);
+            D2H(ho->req.evictions + ra, so.req.evictions, nb * 4);
+            if (ho->req.f_t) D2H(ho->req.f_t + ra, so.req.f_t, nb * 8);
+            if (ho->req.state) D2H(ho->req.state + ra, so.req.state, nb * 4);
+            D2H(ho->stats + ta, so.stats, (size_t)Ts * sizeof(ss_trace_stats));
+            D2H(ho->unservable_slots + ra, so.unservable_slots, nb * 4);
+            if (logr) D2H(ho->round_log + la, so.round_log, (size_t)lw * 4);
 #undef D2H
+        }
+        for (int s = 0; s < S; s++) CK(cudaStreamSynchronize(g_stage.streams[s]));
+        return SS_OK;
+    };
+    rc = run_slices();
+    if (rc) {
+        for (int s = 0; s < S; s++)
+            if (g_stage.streams[s]) cudaStreamSynchronize(g_stage.streams[s]);
+        drop_events();
+        return rc;
     }
-    for (int s = 0; s < S; s++) CK(cudaStreamSynchronize(g_stage.streams[s]));
-    cudaEventDestroy(ev_in);
     if (kernel_ms && S > 1) {
         // span from the first slice's prepass to the last kernel to finish
         float mx = 0.f;
         for (int s = 0; s < S; s++) {
             float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, ev_k0, ev_k1[s]));
-            mx = ms > mx ? ms : mx;
-            cudaEventDestroy(ev_k1[s]);
+            if (cudaEventElapsedTime(&ms, ev_k0, ev_k1[s]) == cudaSuccess) mx = ms > mx ? ms : mx;
         }
-        cudaEventDestroy(ev_k0);
         *kernel_ms = g_kernel_ms = mx;
         g_prepass_ms = 0.f;
     }
+    drop_events();
     for (int32_t t = 0; t < T; t++)
         if (ho->stats[t].status != SS_TRACE_OK) return fail(SS_ERR_TRACE_FAILED, "a trace ended with a non-OK status");
     return SS_OK;

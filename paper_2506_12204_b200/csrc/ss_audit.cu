@@ -185,6 +185,7 @@ size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 std::mutex g_mu;
 void* g_buf = nullptr;
 size_t g_cap = 0;
+int g_dev = -1;  // device g_buf lives on
 thread_local double g_rows_ms = 0.0;
 
 }  // namespace
@@ -220,6 +221,16 @@ int ss_audit_host(int32_t n_traces, const int64_t* offsets, const double* finish
     size_t need = a16((T + 1) * 8) + 2 * a16(nn * 8) + a16(nn * 4) + a16(nn * 8) + 4 * a16(T * 8) +
                   3 * a16(nn * 4) + a16(nn * 8);
     std::lock_guard<std::mutex> lk(g_mu);
+    int cur = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess) return fail(SS_ERR_CUDA, "cudaGetDevice");
+    if (g_buf && g_dev != cur) {  // the caller moved to another device: release on the old one
+        cudaSetDevice(g_dev);
+        cudaFree(g_buf);
+        cudaSetDevice(cur);
+        g_buf = nullptr;
+        g_cap = 0;
+    }
+    g_dev = cur;
     if (g_cap < need) {
         if (g_buf) cudaFree(g_buf);
         g_buf = nullptr;
@@ -267,6 +278,7 @@ int ss_audit_host(int32_t n_traces, const int64_t* offsets, const double* finish
     cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
     if (yb > 0) audit_rows<<<dim3((unsigned)T, yb), AT, 0, st>>>(in, d_v, d_c, d_rv, d_rk, want ? 1 : 0);
+    cudaError_t le = cudaGetLastError();
     cudaEventRecord(e1, st);
     cudaMemcpyAsync(violations, d_v, T * 8, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(comparable, d_c, T * 8, cudaMemcpyDeviceToHost, st);
@@ -276,6 +288,7 @@ int ss_audit_host(int32_t n_traces, const int64_t* offsets, const double* finish
     g_rows_ms = ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (le != cudaSuccess) return fail(SS_ERR_CUDA, cudaGetErrorString(le));
     if (e != cudaSuccess) return fail(SS_ERR_CUDA, cudaGetErrorString(e));
     if (!want) return SS_OK;
     int64_t total = 0;
@@ -300,8 +313,10 @@ int ss_audit_host(int32_t n_traces, const int64_t* offsets, const double* finish
     audit_scatter<<<(unsigned)T, 256, 0, st>>>(in, d_rv, d_rk, d_byr, d_cr);
     audit_scan<<<(unsigned)T, 1024, 0, st>>>(in, d_nc, d_cr, d_base, d_pos);
     audit_pairs<<<dim3((unsigned)T, yb), AT, 0, st>>>(in, d_id, d_nc, d_byr, d_pos, d_pairs);
+    le = cudaGetLastError();
     cudaMemcpyAsync(pairs, d_pairs, (size_t)total * 16, cudaMemcpyDeviceToHost, st);
     e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = le;
     cudaFree(d_byr);
     cudaFree(d_pairs);
     if (e != cudaSuccess) return fail(SS_ERR_CUDA, cudaGetErrorString(e));

@@ -2075,6 +2075,12 @@ int launch_sched(const KArgs& a, int blocks, void* stream) {
     const void* k = kernel_for(a.P.policy, mode);
     if (!k) return SS_ERR_UNSUPPORTED;
     void* argv[] = {(void*)&a};
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (smem > (size_t)optin) return SS_ERR_UNSUPPORTED;  // SS_WPB x per-warp state exceeds the SM
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return SS_ERR_CUDA;
     if (a.P.policy == SS_POLICY_SEMANTIC) {  // the chunked variants first; the unselected ones exit at once
         for (int v : {12, 4}) {
             const void* kc = kernel_for(a.P.policy, mode | v);

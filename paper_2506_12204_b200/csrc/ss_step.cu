@@ -396,7 +396,8 @@ struct Stage {
     std::mutex mu;
     void* buf = nullptr;
     size_t cap = 0;
-    void* host = nullptr;  // pinned bounce buffer
+    int dev = -1;          // device `buf` lives on
+    void* host = nullptr;  // pinned bounce buffer (portable across devices)
     size_t hcap = 0;
 };
 Stage g_sel, g_ev;
@@ -404,6 +405,16 @@ Stage g_sel, g_ev;
 size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 int ensure(Stage& s, size_t dev, size_t host) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess) return fail(SS_ERR_CUDA, "cudaGetDevice");
+    if (s.buf && s.dev != cur) {  // the caller moved to another device: release on the old one
+        cudaSetDevice(s.dev);
+        cudaFree(s.buf);
+        cudaSetDevice(cur);
+        s.buf = nullptr;
+        s.cap = 0;
+    }
+    s.dev = cur;
     if (s.cap < dev) {
         if (s.buf) cudaFree(s.buf);
         s.buf = nullptr;
@@ -497,8 +508,10 @@ int ss_select_batch(const ss_key4* stored, const ss_key4* current, const uint8_t
         a.n_part = nwarps * 32;
     }
     sel_final<<<1, 32, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SS_ERR_CUDA, cudaGetErrorString(e));
     cudaMemcpyAsync(g_sel.host, d_out, out_words * 4, cudaMemcpyDeviceToHost, st);
-    cudaError_t e = cudaStreamSynchronize(st);
+    e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fail(SS_ERR_CUDA, cudaGetErrorString(e));
     const int* o = (const int*)g_sel.host;
     if (n_cand) *n_cand = o[0];
@@ -577,8 +590,10 @@ int ss_evict(const ss_key4* ev_keys, const uint32_t* prompt, const uint32_t* pre
     a.skipped = d_sk;
     a.counts = d_c;
     evict_kernel<<<1, 32, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SS_ERR_CUDA, cudaGetErrorString(e));
     cudaMemcpyAsync(g_ev.host, d_c, 3 * 8, cudaMemcpyDeviceToHost, st);
-    cudaError_t e = cudaStreamSynchronize(st);
+    e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fail(SS_ERR_CUDA, cudaGetErrorString(e));
     const long long* c = (const long long*)g_ev.host;
     if (c[0] > 0) cudaMemcpy(victims, d_v, (size_t)c[0] * sizeof(ss_victim), cudaMemcpyDeviceToHost);

@@ -74,3 +74,41 @@ def test_shard_seeds_partition():
     parts = [shard_seeds(4096, r) for r in range(8)]
     allv = np.concatenate(parts)
     assert np.array_equal(allv, np.arange(8 * 4096))
+
+
+def _bench_dry(nproc, traces):
+    import json
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, os.path.join(repo, "bench.py"), "--dry", "--workload", "E", "--traces", str(traces),
+           "--gpus", str(nproc)]
+    if nproc > 1:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}"] + cmd[1:]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=repo)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_bench_config_e_sharding_gathers_one_job():
+    """bench.py --workload E under torchrun (2 ranks, gloo): one fixed job
+    split in seed blocks, every trace's record gathered once, in seed order,
+    identical to a single-process run."""
+    two = _bench_dry(2, 512)
+    one = _bench_dry(1, 512)
+    assert two["gathered_traces"] == one["gathered_traces"] == two["traces_total"] == 512
+    assert two["seeds_in_order"] and one["seeds_in_order"]
+    assert two["checksum"] == one["checksum"]
+
+
+def test_job_seeds_blocks():
+    from paper_2506_12204_b200.dist import job_seeds
+
+    for total, world in ((65536, 8), (65536, 2), (10, 3), (5, 8)):
+        parts = [job_seeds(total, world, r) for r in range(world)]
+        assert np.array_equal(np.concatenate(parts), np.arange(total))
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
