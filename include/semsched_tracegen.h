@@ -64,6 +64,25 @@ int ss_generate_traces(const ss_gen_spec* spec, int64_t n_traces, const int64_t*
 int ss_generate_traces_device(const ss_gen_spec* spec, int64_t n_traces, const int64_t* seeds,
                               const int64_t* pred_seeds, const ss_gen_out* out, void* stream);
 
+/* One trace's arrivals as workload.generate(spec) with Random(seed)
+ * (workload.py:63-93): N = spec->total_requests requests in generation order
+ * (id = index). Only the workload fields of `spec` are read (bucket_reps must
+ * be non-NULL). Returns 0 on success, 1 on an invalid spec. */
+int ss_generate_arrivals(const ss_gen_spec* spec, int64_t seed, double* arrival, uint32_t* prompt,
+                         uint32_t* true_out, uint8_t* true_urg);
+
+/* predictors.predictor_pipeline (predictors.py:85-149) over n time-ordered
+ * requests, continuing the caller's CPython Random: `mt_state` holds the 624
+ * MT19937 words and the position (Random.getstate()[1]) and is advanced in
+ * place. `what`: bit 0 urgency predictions (pred_urg, spec levels /
+ * urgency_error / urgency_disp), bit 1 length buckets (pred_bucket: bucket
+ * index; max_output_len / buckets / length_error / length_disp), bit 2 the
+ * FIFO prediction server's ready times (latency_s, pred_batch,
+ * full_batching). Returns 0 on success, 1 on invalid arguments. */
+int ss_predict(const ss_gen_spec* spec, int64_t n, const double* arrival, const uint32_t* true_out,
+               const uint8_t* true_urg, int32_t what, uint32_t* mt_state, uint8_t* pred_urg,
+               uint32_t* pred_bucket, double* ready);
+
 #ifdef __cplusplus
 }
 #endif

@@ -134,12 +134,9 @@ int bisect_right(const double* cum, double x, int hi) {
     return lo;
 }
 
-void gen_one(const ss_gen_spec& S, int64_t seed, int64_t pred_seed, int64_t off, const ss_gen_out& O) {
+// workload.generate: N requests in generation (= record) order
+void gen_arrivals(const ss_gen_spec& S, MT& g, Req* rq) {
     const int64_t N = S.total_requests;
-    std::vector<Req> rq((size_t)N);
-    MT g;
-    // ---- workload.generate
-    g.seed(seed);
     std::vector<double> cum((size_t)S.levels);
     double acc = 0.0;
     for (int l = 0; l < S.levels; l++) {
@@ -156,7 +153,7 @@ void gen_one(const ss_gen_spec& S, int64_t seed, int64_t pred_seed, int64_t off,
             int u = bisect_right(cum.data(), g.random() * total, S.levels - 1);
             int64_t pl = g.randint(S.prompt_lo, S.prompt_hi);
             int64_t ol = g.randint(S.out_lo, S.out_hi);
-            Req& r = rq[(size_t)placed];
+            Req& r = rq[placed];
             r.id = placed;
             r.arrival = t;
             r.prompt = (uint32_t)pl;
@@ -166,42 +163,51 @@ void gen_one(const ss_gen_spec& S, int64_t seed, int64_t pred_seed, int64_t off,
         }
         tick++;
     }
-    // ---- predictors.predictor_pipeline
-    MT p;
-    p.seed(pred_seed);
-    std::vector<uint8_t> fe((size_t)N);
-    std::vector<uint32_t> mid((size_t)N);
-    auto displace = [&](int64_t value, int64_t lo, int64_t hi, int64_t d) {
-        int64_t step = p.random() < 0.5 ? d : -d;
-        int64_t o = std::min(hi, std::max(lo, value + step));
-        if (o == value) o = std::min(hi, std::max(lo, value - step));
-        return o;
-    };
+}
+
+// Error-model displacement: +-d with a drawn sign, clamped; the other sign
+// when clamping would leave the value unchanged.
+int64_t displace(MT& p, int64_t value, int64_t lo, int64_t hi, int64_t d) {
+    int64_t step = p.random() < 0.5 ? d : -d;
+    int64_t o = std::min(hi, std::max(lo, value + step));
+    if (o == value) o = std::min(hi, std::max(lo, value - step));
+    return o;
+}
+
+// predictors.predictor_pipeline over N time-ordered requests: per request the
+// urgency draw(s) then the length draw(s) (`what` bit 0 / bit 1), then the
+// single FIFO prediction server's ready times (bit 2). fe: predicted rank,
+// bucket: predicted length bucket index.
+void predict(const ss_gen_spec& S, MT& p, int64_t N, const Req* rq, int what, uint8_t* fe, uint32_t* bucket,
+             double* ready) {
     for (int64_t i = 0; i < N; i++) {
-        Req& r = rq[(size_t)i];
-        int64_t u = r.urg;
-        if (!(p.random() >= S.urgency_error)) u = displace(u, 0, S.levels - 1, S.urgency_disp);
-        int64_t len = r.out;
-        if (p.random() < S.length_error) len = displace(len, 0, S.max_output_len, S.length_disp);
-        if (len > S.max_output_len) len = S.max_output_len;
-        int64_t idx = std::min<int64_t>(S.buckets - 1, (len * S.buckets) / S.max_output_len);
-        fe[(size_t)i] = (uint8_t)u;
-        mid[(size_t)i] = S.bucket_reps[idx];
+        const Req& r = rq[i];
+        if (what & 1) {
+            int64_t u = r.urg;
+            if (!(p.random() >= S.urgency_error)) u = displace(p, u, 0, S.levels - 1, S.urgency_disp);
+            fe[i] = (uint8_t)u;
+        }
+        if (what & 2) {
+            int64_t len = r.out;
+            if (p.random() < S.length_error) len = displace(p, len, 0, S.max_output_len, S.length_disp);
+            if (len > S.max_output_len) len = S.max_output_len;
+            bucket[i] = (uint32_t)std::min<int64_t>(S.buckets - 1, (len * S.buckets) / S.max_output_len);
+        }
     }
-    std::vector<double> ready((size_t)N);
+    if (!(what & 4)) return;
     double free_at = 0.0;
     auto serve = [&](int64_t a, int64_t b, double filled) {
         double start = filled >= free_at ? filled : free_at;  // max(fill_time, server_free)
         double done = start + S.latency_s;
         free_at = done;
-        for (int64_t i = a; i < b; i++) ready[(size_t)i] = done;
+        for (int64_t i = a; i < b; i++) ready[i] = done;
     };
     if (!S.full_batching) {
         int64_t i = 0;
         while (i < N) {
-            double t = rq[(size_t)i].arrival;
+            double t = rq[i].arrival;
             int64_t j = i;
-            while (j < N && rq[(size_t)j].arrival == t) j++;
+            while (j < N && rq[j].arrival == t) j++;
             for (int64_t k = i; k < j; k += S.pred_batch) serve(k, std::min(j, k + S.pred_batch), t);
             i = j;
         }
@@ -209,12 +215,26 @@ void gen_one(const ss_gen_spec& S, int64_t seed, int64_t pred_seed, int64_t off,
         int64_t start = 0;
         for (int64_t i = 0; i < N; i++) {
             if (i + 1 - start >= S.pred_batch) {
-                serve(start, i + 1, rq[(size_t)i].arrival);
+                serve(start, i + 1, rq[i].arrival);
                 start = i + 1;
             }
         }
-        if (start < N) serve(start, N, rq[(size_t)N - 1].arrival);
+        if (start < N) serve(start, N, rq[N - 1].arrival);
     }
+}
+
+void gen_one(const ss_gen_spec& S, int64_t seed, int64_t pred_seed, int64_t off, const ss_gen_out& O) {
+    const int64_t N = S.total_requests;
+    std::vector<Req> rq((size_t)N);
+    MT g;
+    g.seed(seed);
+    gen_arrivals(S, g, rq.data());
+    MT p;
+    p.seed(pred_seed);
+    std::vector<uint8_t> fe((size_t)N);
+    std::vector<uint32_t> bucket((size_t)N);
+    std::vector<double> ready((size_t)N);
+    predict(S, p, N, rq.data(), 7, fe.data(), bucket.data(), ready.data());
     // pending order: (ready, arrival, id); generate() ids ascend with arrival
     std::vector<int64_t> ord((size_t)N);
     for (int64_t i = 0; i < N; i++) ord[(size_t)i] = i;
@@ -231,7 +251,7 @@ void gen_one(const ss_gen_spec& S, int64_t seed, int64_t pred_seed, int64_t off,
         O.arrival[g2] = r.arrival;
         O.prompt[g2] = r.prompt;
         O.true_out[g2] = r.out;
-        O.pred_len[g2] = mid[(size_t)i];
+        O.pred_len[g2] = S.bucket_reps[bucket[(size_t)i]];
         O.pred_urg[g2] = fe[(size_t)i];
         O.true_urg[g2] = r.urg;
         O.tie[g2] = (uint32_t)i;  // rank of (arrival, id): the generation order
@@ -240,16 +260,19 @@ void gen_one(const ss_gen_spec& S, int64_t seed, int64_t pred_seed, int64_t off,
     }
 }
 
+bool spec_ok(const ss_gen_spec& S) {
+    return !(S.total_requests < 0 || S.levels < 1 || S.levels > 255 || S.concurrent < 1 || S.buckets < 1 ||
+             S.max_output_len < 1 || S.pred_batch < 1 || S.out_hi > S.max_output_len || S.prompt_lo < 1 ||
+             S.out_lo < 1 || !S.bucket_reps);
+}
+
 }  // namespace
 
 extern "C" int ss_generate_traces(const ss_gen_spec* spec, int64_t n_traces, const int64_t* seeds,
                                   const int64_t* pred_seeds, const ss_gen_out* out, int n_threads) {
     if (!spec || !out || (n_traces > 0 && (!seeds || !pred_seeds))) return 1;
     const ss_gen_spec S = *spec;
-    if (S.total_requests < 0 || S.levels < 1 || S.levels > 255 || S.concurrent < 1 || S.buckets < 1 ||
-        S.max_output_len < 1 || S.pred_batch < 1 || S.out_hi > S.max_output_len || S.prompt_lo < 1 ||
-        S.out_lo < 1 || !S.bucket_reps)
-        return 1;
+    if (!spec_ok(S)) return 1;
     std::atomic<int64_t> next(0);
     auto work = [&]() {
         for (;;) {
@@ -265,5 +288,49 @@ extern "C" int ss_generate_traces(const ss_gen_spec* spec, int64_t n_traces, con
     for (int i = 1; i < nt; i++) th.emplace_back(work);
     work();
     for (auto& x : th) x.join();
+    return 0;
+}
+
+extern "C" int ss_generate_arrivals(const ss_gen_spec* spec, int64_t seed, double* arrival, uint32_t* prompt,
+                                    uint32_t* true_out, uint8_t* true_urg) {
+    if (!spec || !spec_ok(*spec)) return 1;
+    const int64_t N = spec->total_requests;
+    if (N > 0 && (!arrival || !prompt || !true_out || !true_urg)) return 1;
+    std::vector<Req> rq((size_t)N);
+    MT g;
+    g.seed(seed);
+    gen_arrivals(*spec, g, rq.data());
+    for (int64_t i = 0; i < N; i++) {
+        arrival[i] = rq[(size_t)i].arrival;
+        prompt[i] = rq[(size_t)i].prompt;
+        true_out[i] = rq[(size_t)i].out;
+        true_urg[i] = rq[(size_t)i].urg;
+    }
+    return 0;
+}
+
+extern "C" int ss_predict(const ss_gen_spec* spec, int64_t n, const double* arrival, const uint32_t* true_out,
+                          const uint8_t* true_urg, int32_t what, uint32_t* mt_state, uint8_t* pred_urg,
+                          uint32_t* pred_bucket, double* ready) {
+    if (!spec || !mt_state || n < 0 || (what & ~7) || spec->levels < 1 || spec->levels > 255 || spec->buckets < 1 ||
+        spec->max_output_len < 1 || spec->pred_batch < 1)
+        return 1;
+    if (n > 0 && (((what & 1) && (!true_urg || !pred_urg)) || ((what & 2) && (!true_out || !pred_bucket)) ||
+                  ((what & 4) && (!arrival || !ready))))
+        return 1;
+    if (mt_state[624] > 624) return 1;
+    std::vector<Req> rq((size_t)n);
+    for (int64_t i = 0; i < n; i++) {
+        rq[(size_t)i].id = i;
+        rq[(size_t)i].arrival = arrival ? arrival[i] : 0.0;
+        rq[(size_t)i].out = true_out ? true_out[i] : 0u;
+        rq[(size_t)i].urg = true_urg ? true_urg[i] : 0u;
+    }
+    MT p;
+    memcpy(p.mt, mt_state, sizeof p.mt);
+    p.mti = (int)mt_state[624];
+    predict(*spec, p, n, rq.data(), what, pred_urg, pred_bucket, ready);
+    memcpy(mt_state, p.mt, sizeof p.mt);
+    mt_state[624] = (uint32_t)p.mti;
     return 0;
 }

@@ -75,6 +75,52 @@ def _gen_spec(spec: WorkloadSpec, predictor: PredictorConfig):
     return s, (reps, weights)
 
 
+def _typed(L, name, argtypes):
+    f = getattr(L, name)
+    if not getattr(f, "_ss_typed", False):
+        f.restype = C.c_int
+        f.argtypes = argtypes
+        f._ss_typed = True
+    return f
+
+
+def native_arrivals(spec: WorkloadSpec):
+    """workload.generate's draws for one spec (ss_generate_arrivals): arrival,
+    prompt, true output and true urgency arrays in generation order."""
+    n = int(spec.total_requests)
+    s, keep = _gen_spec(spec, PredictorConfig())
+    out = (np.empty(n, np.float64), np.empty(n, np.uint32), np.empty(n, np.uint32), np.empty(n, np.uint8))
+    f = _typed(_lib(), "ss_generate_arrivals", [C.POINTER(ss_gen_spec), C.c_int64] + [C.c_void_p] * 4)
+    if f(C.byref(s), int(spec.seed), *[a.ctypes.data if n else None for a in out]):
+        raise ValueError("invalid workload spec for the native generator")
+    return out
+
+
+def native_predict(rng, what: int, levels: int, buckets: int, max_output_len: int, urgency_error: float = 0.0,
+                   length_error: float = 0.0, latency_s: float = 0.0, pred_batch: int = 64,
+                   full_batching: bool = False, arrival=None, true_out=None, true_urg=None, n: int = 0):
+    """The predictor draws of ss_predict, continuing (and advancing) the
+    CPython ``random.Random`` ``rng``: returns (pred_urg, pred_bucket, ready)."""
+    version, words, gauss = rng.getstate()
+    state = np.array(words, dtype=np.uint32)
+    s = ss_gen_spec()
+    s.levels, s.buckets, s.max_output_len = int(levels), int(buckets), int(max_output_len)
+    s.urgency_error, s.length_error = float(urgency_error), float(length_error)
+    s.urgency_disp = ErrorModel(urgency_error, levels).displacement if what & 1 else 1
+    s.length_disp = ErrorModel(length_error, max_output_len).displacement if what & 2 else 1
+    s.latency_s, s.pred_batch, s.full_batching = float(latency_s), int(pred_batch), 1 if full_batching else 0
+    arr = lambda x, dt: np.ascontiguousarray(np.asarray(x, dt)) if x is not None else None
+    a, o, u = arr(arrival, np.float64), arr(true_out, np.uint32), arr(true_urg, np.uint8)
+    pu, pb, rd = np.zeros(n, np.uint8), np.zeros(n, np.uint32), np.zeros(n, np.float64)
+    ptr = lambda x: x.ctypes.data if x is not None and x.size else None
+    f = _typed(_lib(), "ss_predict", [C.POINTER(ss_gen_spec), C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p])
+    if f(C.byref(s), n, ptr(a), ptr(o), ptr(u), int(what), state.ctypes.data, ptr(pu), ptr(pb), ptr(rd)):
+        raise ValueError("invalid predictor arguments")
+    rng.setstate((version, tuple(int(w) for w in state), gauss))
+    return pu, pb, rd
+
+
 def generate_batch_device(spec: WorkloadSpec, seeds: Sequence[int], predictor: PredictorConfig = PredictorConfig(),
                           pred_seeds: Sequence[int] = None, device="cuda"):
     """``generate_batch`` on the GPU (``ss_generate_traces_device``, one thread

@@ -159,6 +159,75 @@ def test_generate_matches_reference_package():
                    [(r.id, r.arrival_time, r.prompt_len, r.true_output_len, r.true_urgency.rank) for r in ref]
 
 
+@pytest.mark.skipif(not has_reference(), reason="reference not mounted (GPU box)")
+def test_predictors_match_reference_package():
+    """Native predictor draws on the caller's Random: same predictions, same
+    ready times and the caller's stream left where the reference leaves it."""
+    import random
+    import sys
+
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from semsched import predictors as RP
+    from semsched.requests import UrgencyLevel as RU
+    from semsched.workload import WorkloadSpec as RW, generate as rgen
+    from paper_2506_12204_b200 import predictors as MP
+
+    for seed, kw in ((3, dict(urgency_error=0.4, length_error=0.3)),
+                     (5, dict(latency_s=0.05, batch_size=3, strategy="full_batching", urgency_error=1.0)),
+                     (9, dict(latency_s=0.3, batch_size=2, length_error=0.9))):
+        spec = dict(total_requests=150, seed=seed, levels=4, concurrent=6)
+        mine, ref = generate(WorkloadSpec(**spec)), rgen(RW(**spec))
+        mk = {**kw, "strategy": Strategy(kw.get("strategy", "immediate"))}
+        rk = {**kw, "strategy": RP.Strategy(kw.get("strategy", "immediate"))}
+        r1, r2 = random.Random(seed), random.Random(seed)
+        a = MP.predictor_pipeline(mine, PredictorConfig(**mk), r1, levels=4)
+        b = RP.predictor_pipeline(ref, RP.PredictorConfig(**rk), r2, levels=4)
+        assert [(t, r.id, r.f_e.rank, r.predicted_bucket.index, r.predicted_bucket.representative_len)
+                for t, r in a] == [(t, r.id, r.f_e.rank, r.predicted_bucket.index,
+                                    r.predicted_bucket.representative_len) for t, r in b]
+        assert r1.getstate() == r2.getstate()
+    # the single-request API
+    r1, r2 = random.Random(11), random.Random(11)
+    for k in range(300):
+        em_m, em_r = MP.ErrorModel(0.5, 5), RP.ErrorModel(0.5, 5)
+        assert MP.predict_urgency(UrgencyLevel(k % 5, 5), em_m, r1).rank == \
+            RP.predict_urgency(RU(k % 5, 5), em_r, r2).rank
+    assert r1.getstate() == r2.getstate()
+    r1, r2 = random.Random(12), random.Random(12)
+    for k in range(300):
+        x = MP.predict_length_bucket(k, MP.ErrorModel(0.3, 400), r1, 7)
+        y = RP.predict_length_bucket(k, RP.ErrorModel(0.3, 400), r2, 7)
+        assert (x.index, x.representative_len) == (y.index, y.representative_len)
+    assert r1.getstate() == r2.getstate()
+
+
+@pytest.mark.skipif(not has_reference(), reason="reference not mounted (GPU box)")
+def test_load_dataset_matches_reference_package(tmp_path):
+    import json
+    import sys
+
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from semsched.workload import WorkloadSpec as RW, load_dataset as rload
+    from paper_2506_12204_b200.workload import load_dataset
+
+    lines = [json.dumps({"id": i, "prompt_tokens": 10 + i, "urgency": i % 3, "output_tokens": 5 + i}) for i in range(40)]
+    lines[3] = "{not json"
+    lines[7] = json.dumps({"id": 7, "urgency": 9, "output_tokens": 4, "prompt_tokens": 3})
+    lines[9] = json.dumps({"id": 9, "urgency": 1, "output_tokens": 4, "prompt": "a b c d"})
+    lines[11] = json.dumps({"id": 11, "urgency": 1, "output_tokens": 4})
+    lines[12] = json.dumps({"urgency": 1, "output_tokens": 4})
+    lines[13] = json.dumps({"id": 13, "urgency": 1, "output_tokens": 0, "prompt_tokens": 2})
+    lines[14] = ""
+    p = tmp_path / "d.jsonl"
+    p.write_text("\n".join(lines) + "\n")
+    for kw in (dict(levels=3, seed=4), dict(levels=3, seed=5, concurrent=3, concurrent_mode="fixed", gap_s=0.5)):
+        a, ea = load_dataset(str(p), WorkloadSpec(**kw))
+        b, eb = rload(str(p), RW(**kw))
+        assert ea == eb
+        assert [(r.id, r.arrival_time, r.prompt_len, r.true_output_len, r.true_urgency.rank) for r in a] == \
+               [(r.id, r.arrival_time, r.prompt_len, r.true_output_len, r.true_urgency.rank) for r in b]
+
+
 # ---- the C-ABI library: loads without a GPU and exports every declared symbol
 def _declared_symbols():
     syms = set()
