@@ -681,7 +681,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
     // MODE bit 4: decode_batch_cost "sum" (Neumaier sum of the members' decode steps)
     // compiled in; the other kernels carry only the "max" batch duration
     constexpr bool sum_k = (MODE & 16) != 0;
+#ifdef SS_LEAN_TEST  // experiment: timing without the stale-entry machinery (wrong on anomaly traces)
+    constexpr bool anom_ok = false;
+#else
     constexpr bool anom_ok = !noev;  // stale heap entries can arise (an eviction can lose its decisions)
+#endif
     const int sel = *A.w.sel;
     if (POL == SS_POLICY_SEMANTIC &&
         sel != (noev ? SS_SEL_NO_EVICT : (chunking ? SS_SEL_CHUNKED : SS_SEL_PERROUND)))
@@ -1394,6 +1398,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             }
             const int nO_start = T.nO;
             const int nuns_start = c.nuns;
+            __syncwarp();  // lane 0 updates Cold fields next to nuns below (racecheck)
             // a completed request popped from a stale entry: estimate_kv_size raises
             if (anom_ok && uni(anom) && __ballot_sync(FULL, act && (mem.flg & F_STAGE) == ST_DONE)) {
                 set_status(T, SS_TRACE_REF_ERROR);

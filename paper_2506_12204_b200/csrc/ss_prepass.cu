@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(PP_THREADS) init_kernel(const __grid_constant_
             A.out.req.first_scheduled[g] = __longlong_as_double(0x7ff8000000000000ll);
             A.out.req.finish_time[g] = __longlong_as_double(0x7ff8000000000000ll);
             A.out.req.evictions[g] = 0u;
+            A.out.unservable_slots[g] = 0xFFFFFFFFu;  // defined contents past the trace's list
             tok = tout;
             foot = (unsigned long long)prompt + (tout > mid ? tout : mid) + 1u;
             uns = serv ? 0u : 1u;

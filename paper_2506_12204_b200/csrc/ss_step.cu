@@ -507,6 +507,7 @@ int ss_select_batch(const ss_key4* stored, const ss_key4* current, const uint8_t
         a.part = d_part;
         a.n_part = nwarps * 32;
     }
+    cudaMemsetAsync(d_out, 0, out_words * 4, st);  // words past the lists are copied back too
     sel_final<<<1, 32, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SS_ERR_CUDA, cudaGetErrorString(e));

@@ -26,7 +26,7 @@ METRICS = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "dram__bytes_rea
            "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg",
            "smsp__warps_active.avg.per_cycle_active", "launch__registers_per_thread"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
-         "second": 1.0}
+         "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
 
 
 def profile(w: str) -> dict:

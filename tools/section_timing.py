@@ -11,7 +11,7 @@ from paper_2506_12204_b200.results import make_params
 W = sys.argv[1]
 wl = bench.WORKLOADS[W]
 T = int(sys.argv[2]) if len(sys.argv) > 2 else wl["traces"]
-batch, T = bench.build_batch(wl, 0, T, pinned=False)
+batch = bench.native_batch(W, wl, np.arange(T), pinned=False)
 prm = make_params(get_profile(wl["profile"]), 16, wl["capacity"], levels=wl["levels"], flags=A.SS_FLAG_DIGEST)
 lib = native.lib()
 buf = (C.c_ulonglong * 24)()
