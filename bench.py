@@ -229,13 +229,17 @@ def reference_batch(name, wl, seeds):
     return TraceBatch.concat(parts)
 
 
+VARIANT = os.environ.get("SS_BENCH_VARIANT", "auto")  # dev: force a scheduler variant
+
+
 def params_for(wl, flags=None):
     from paper_2506_12204_b200 import _abi as A
     from paper_2506_12204_b200.costs import get_profile
     from paper_2506_12204_b200.results import make_params
 
+    force = {"auto": 0, "chunked": A.SS_FLAG_FORCE_CHUNKED, "perround": A.SS_FLAG_FORCE_PERROUND}[VARIANT]
     return make_params(get_profile(wl["profile"]), 16, wl["capacity"], levels=wl["levels"],
-                       flags=A.SS_FLAG_DIGEST if flags is None else flags)
+                       flags=(A.SS_FLAG_DIGEST if flags is None else flags) | force)
 
 
 # ------------------------------------------------------------- CPU legs -----

@@ -865,7 +865,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     // per-membership values, recomputed when members complete
                     int left;                 // rounds before the first completion (dec + 1 >= tout)
                     unsigned nmax;            // longest context + 1 (decode step of the batch)
-                    long long safe_used;      // no member needs an eviction while used <= this
+                    long long safe_used;      // per-round kernels: no member evicts while used <= this
+                    int evleft;               // chunked kernels: rounds before the first one that evicts
                     unsigned long long gt;    // this lane's grant term (ss_grant_term of its batch position)
                     unsigned long long hb;    // chunked kernels: the batch list's hash (sum of the grant terms)
                     // header lanes 29..31: tag pre-multiplied (ss_term); round multiplier of the grant terms
@@ -878,11 +879,30 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         // KV admission (engine.py:296-327) of an all-decode batch: immediate 1,
                         // exclusive scan = lane, demand = max(est, 1), est non-increasing
                         if (noev) {
-                            safe_used = 0x7fffffffffffffffll;  // no eviction possible
-                        } else {
+                            evleft = 0x7fffffff;  // no eviction possible
+                            safe_used = 0x7fffffffffffffffll;
+                        } else if (!chunking) {
                             const long long est0 = act ? (long long)m_mid(mem) - (long long)mem.dec : 0;
                             const int maxdem = (int)__reduce_max_sync(FULL, (unsigned)(est0 > 1 ? est0 : 1));
                             safe_used = cap - (long long)maxdem - m;
+                        } else {
+                            // round j (from now) evicts iff some member i has demand_i(j) + i +
+                            // used + j*m > cap, demand_i(j) = max(mid - dec - j, 1) (or 1 when
+                            // demand + i > cap). Monotone in j: count the safe rounds by binary
+                            // lifting per member, then the minimum over the members.
+                            const long long e0 = (long long)m_mid(mem) - (long long)mem.dec;
+                            const long long room = cap - T.used;
+                            auto evicts = [&](int j) {
+                                const long long e = e0 - j;
+                                long long dm = e > 1 ? e : 1;
+                                if (dm + lane > cap) dm = 1;
+                                return dm + lane + (long long)j * m > room;
+                            };
+                            int safe = 0;
+#pragma unroll 1
+                            for (int st = 2048; st > 0; st >>= 1)
+                                safe += evicts(safe + st - 1) ? 0 : st;
+                            evleft = __reduce_min_sync(FULL, act ? safe : 0x7fffffff);
                         }
                         gt = act ? ss_grant_term((uint32_t)lane, mem.slot) : 0ull;
                         if (chunking) hb = warp_sum_u64(gt);
@@ -911,7 +931,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             if (!uni((left <= 0) & !adm & !capx) || !__any_sync(FULL, pdec)) break;
                             cround = true;
                         }
-                        if (!noev && uni(T.used > safe_used)) {
+                        if (!noev && chunking && uni(evleft <= 0)) break;  // this round's admission evicts
+                        if (!noev && !chunking && uni(T.used > safe_used)) {
                             long long e = (long long)m_mid(mem) - (long long)mem.dec;
                             long long dem = e > 1 ? e : 1;
                             if (dem + lane > cap) dem = 1;
@@ -931,7 +952,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
 #ifndef SS_NO_CHUNK
                         if (chunking && !cround && !sum_mode) {
                             chunk = left >= SS_CHUNK_MIN && T.rounds + (SS_CHUNK_MIN - 1) < round_cap &&
-                                    (noev || T.used + (long long)(SS_CHUNK_MIN - 1) * m <= safe_used);
+                                    evleft >= SS_CHUNK_MIN;
                             if (logging)
                                 chunk = chunk && c.logpos + (long long)(SS_CHUNK_MIN - 1) * (SS_LOG_HEADER_WORDS + m) <=
                                                      c.logcap;
@@ -1029,6 +1050,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         T.rounds += 1;
                         nmax += 1u;
                         left -= 1;
+                        evleft -= 1;
                         k += 1;
                         spool += live_s;
                         sgr += m;
@@ -1112,7 +1134,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             // (completion, round cap, memory safety, log space) stops it
                             const bool adm_j = T.next_ready <= ss::add(befj, 1e-12);
                             bool lim = (lane >= L) | (T.rounds + lane >= round_cap);
-                            if (!noev) lim |= T.used + (long long)lane * m > safe_used;
+                            if (!noev) lim |= lane >= evleft;
                             if (logging) lim |= c.logpos + (long long)lane * (SS_LOG_HEADER_WORDS + m) > c.logcap;
                             const unsigned stop = __ballot_sync(FULL, lim | adm_j) |
                                                   (__ballot_sync(FULL, !(pk & ok)) << 1);
@@ -1161,6 +1183,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             T.rounds += Lx;
                             nmax += (unsigned)Lx;
                             left -= Lx;
+                            evleft -= Lx;
                             k += Lx;
                             spool += (long long)Lx * live_s;
                             sgr += (long long)Lx * m;

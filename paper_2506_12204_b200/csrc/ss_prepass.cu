@@ -188,24 +188,53 @@ __global__ void __launch_bounds__(PP_THREADS) init_kernel(const __grid_constant_
     }
 }
 
-// ---- 2b. scheduler variant: chunked stretches only where the KV budget can never
-// bind (twice the largest per-trace footprint bound fits), i.e. no trace can
-// ever evict; tight budgets keep the per-round variant (shorter stretches).
+#ifndef SS_CHUNK_TIGHTNESS
+#define SS_CHUNK_TIGHTNESS 0.55  // KV budget / (b x mean footprint bound) above which chunks run
+#endif
+
+// ---- 2b. scheduler variant: the no-eviction chunked kernel where the KV budget
+// can never bind (twice the largest per-trace footprint bound fits), i.e. no
+// trace can ever evict; otherwise the evicting chunked kernel when the budget
+// holds SS_CHUNK_TIGHTNESS of a full batch's mean footprint, else the
+// per-round kernel (heavy eviction: short stretches).
 __global__ void __launch_bounds__(1024) select_kernel(const __grid_constant__ KArgs A) {
     __shared__ unsigned long long wmax[32];
+    __shared__ double wfoot[32], wn[32];
     const int T = A.in.n_traces;
     unsigned long long mx = 0;
-    for (int t = threadIdx.x; t < T; t += blockDim.x) mx = A.w.foot[t] > mx ? A.w.foot[t] : mx;
+    double fs = 0.0, ns = 0.0;  // footprint bounds and requests over all traces
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        mx = A.w.foot[t] > mx ? A.w.foot[t] : mx;
+        fs += (double)A.w.foot[t];
+        ns += (double)(A.in.trace_offsets[t + 1] - A.in.trace_offsets[t]);
+    }
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long y = __shfl_xor_sync(FULL, mx, o);
         mx = y > mx ? y : mx;
+        fs += __shfl_xor_sync(FULL, fs, o);
+        ns += __shfl_xor_sync(FULL, ns, o);
     }
-    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = mx;
+    if ((threadIdx.x & 31) == 0) {
+        wmax[threadIdx.x >> 5] = mx;
+        wfoot[threadIdx.x >> 5] = fs;
+        wn[threadIdx.x >> 5] = ns;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int i = 1; i < (int)(blockDim.x >> 5); i++) mx = wmax[i] > mx ? wmax[i] : mx;
+        for (int i = 1; i < (int)(blockDim.x >> 5); i++) {
+            mx = wmax[i] > mx ? wmax[i] : mx;
+            fs += wfoot[i];
+            ns += wn[i];
+        }
         const long long cap = A.P.memory_capacity;
         int sel = (cap > 0 && mx <= (unsigned long long)cap / 2) ? SS_SEL_NO_EVICT : SS_SEL_PERROUND;
+        // evicting regime: chunks pay when the budget holds most of a full batch's
+        // footprint (config A, ratio ~0.71: chunked 22% faster); under heavy eviction
+        // (config D, ~0.40) stretches are short and the per-round kernel is ahead
+        const double per_req = ns > 0.0 ? fs / ns : 0.0;
+        if (sel == SS_SEL_PERROUND && per_req > 0.0 &&
+            (double)cap >= SS_CHUNK_TIGHTNESS * (double)A.P.batch_size * per_req)
+            sel = SS_SEL_CHUNKED;
         if ((A.P.flags & SS_FLAG_FORCE_CHUNKED) && sel != SS_SEL_NO_EVICT) sel = SS_SEL_CHUNKED;
         if (A.P.flags & SS_FLAG_FORCE_PERROUND) sel = SS_SEL_PERROUND;
         *A.w.sel = sel;
