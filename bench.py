@@ -175,57 +175,50 @@ def native_batch(name, wl, seeds, pinned=True):
     return generate_batch(spec, seeds, pinned=pinned)
 
 
-def _ref_semsched():
-    """The unmodified reference package (baseline/_ref) or None."""
-    if os.path.isdir(os.path.join(REF_PKG, "semsched")):
-        if REF_PKG not in sys.path:
-            sys.path.insert(0, REF_PKG)
-        import semsched  # noqa: F401
+REF_SRC = "/root/reference/pkg/src"  # build container only (absent on the GPU box)
 
-        return semsched
+
+def _ref_semsched():
+    """The unmodified reference package (baseline/_ref, else its source tree
+    when this is the build container) or None."""
+    for root in (REF_PKG, REF_SRC):
+        if os.path.isdir(os.path.join(root, "semsched")):
+            if root not in sys.path:
+                sys.path.insert(0, root)
+            import semsched  # noqa: F401
+
+            return semsched
     return None
 
 
 def reference_batch(name, wl, seeds):
     """Reference-arm inputs WITHOUT this package's CUDA library: the
     reference's own generate + predictor_pipeline (baseline/_ref) laid out
-    as the oracle's SoA; this package's pure-Python restatement when the
-    reference is not installed."""
+    as the oracle's SoA."""
     import random
 
     from paper_2506_12204_b200.soa import TraceBatch, from_prepared
 
     ref = _ref_semsched()
+    if ref is None:
+        raise SystemExit("reference arm: the reference package is not installed (baseline/_ref)")
+    from semsched.predictors import PredictorConfig, predictor_pipeline
+    from semsched.requests import Request, UrgencyLevel
+    from semsched.workload import WorkloadSpec, generate
+
     parts = []
     for s in seeds:
-        if ref is not None:
-            from semsched.predictors import PredictorConfig, predictor_pipeline
-            from semsched.requests import Request, UrgencyLevel
-            from semsched.workload import WorkloadSpec, generate
+        if name == "A":
+            from paper_2506_12204_b200.scenarios import medical_arrivals
 
-            if name == "A":
-                from paper_2506_12204_b200.scenarios import medical_arrivals
-
-                arr = [Request(id=r.id, arrival_time=r.arrival_time, prompt_len=r.prompt_len,
-                               true_output_len=r.true_output_len, true_urgency=UrgencyLevel(r.true_urgency.rank, 3))
-                       for r in medical_arrivals(seed=0, n=wl["requests"])]
-            else:
-                arr = generate(WorkloadSpec(total_requests=wl["requests"], levels=wl["levels"], seed=int(s)))
-            ready = predictor_pipeline(arr, PredictorConfig(), random.Random(0 if name == "A" else int(s)),
-                                       levels=wl["levels"])
-            parts.append(from_prepared(arr, ready))
+            arr = [Request(id=r.id, arrival_time=r.arrival_time, prompt_len=r.prompt_len,
+                           true_output_len=r.true_output_len, true_urgency=UrgencyLevel(r.true_urgency.rank, 3))
+                   for r in medical_arrivals(seed=0, n=wl["requests"])]
         else:
-            from paper_2506_12204_b200.soa import prepare_trace
-            from paper_2506_12204_b200.workload import generate as my_generate
-
-            cfg = scenario(name, wl, 0 if name == "A" else int(s))
-            if name == "A":
-                from paper_2506_12204_b200.scenarios import medical_arrivals
-
-                arr = medical_arrivals(seed=0, n=wl["requests"])
-            else:
-                arr = my_generate(cfg.workload)
-            parts.append(prepare_trace(arr, cfg)[0])
+            arr = generate(WorkloadSpec(total_requests=wl["requests"], levels=wl["levels"], seed=int(s)))
+        ready = predictor_pipeline(arr, PredictorConfig(), random.Random(0 if name == "A" else int(s)),
+                                   levels=wl["levels"])
+        parts.append(from_prepared(arr, ready))
     return TraceBatch.concat(parts)
 
 
