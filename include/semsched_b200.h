@@ -175,7 +175,7 @@ typedef struct ss_request_out {
     uint32_t* generated;        /* RequestRecord.generated_tokens */
     uint32_t* evictions;        /* RequestRecord.evictions        */
     double*   f_t;              /* final Request.f_t  (optional, may be NULL)      */
-    uint32_t* state;            /* final stage | prefilled<<8 (optional, NULL ok)  */
+    uint32_t* state;            /* final stage | prefilled<<8 | unservable-while-decoding<<9 (optional, NULL ok) */
 } ss_request_out;
 
 /* Whole-call outputs. */

@@ -734,7 +734,8 @@ static void run_trace(const ss_params* P, const ss_trace_batch* B, const int64_t
             uint32_t stg = r->unservable ? SS_STAGE_UNSERVABLE
                          : (r->stage == ST_COMPLETED ? SS_STAGE_COMPLETED
                          : (r->stage == ST_DECODING ? SS_STAGE_DECODING : SS_STAGE_WAITING));
-            O->req.state[off + i] = stg | ((r->prefilled > 0 ? 1u : 0u) << 8);
+            O->req.state[off + i] = stg | ((r->prefilled > 0 ? 1u : 0u) << 8) |
+                                    ((r->unservable && r->stage == ST_DECODING ? 1u : 0u) << 9);
         }
         if (!isnan(r->finish)) {
             double w = r->finish - r->arrival;

@@ -7,6 +7,7 @@
 #include <mutex>
 #include <string>
 
+#include "ss_costs.cuh"
 #include "ss_kernel.cuh"
 
 namespace {
@@ -143,6 +144,11 @@ int ss_run_traces(const ss_params* params, const ss_trace_batch* batch, const ss
     a.P = *params;
     a.in = *batch;
     a.out = *out;
+    a.z0 = ss::add(ss::reload_time(0, params->profile), ss::prefill_time(0, params->profile));
+    {
+        const double g1 = params->profile.gamma1, g2 = params->profile.gamma2;
+        a.screen = (g1 >= 0.0 && g2 >= 0.0 && g1 < 1e300 && g2 < 1e300 && a.z0 == 0.0) ? 1 : 0;
+    }
     ss::carve_work(ws, batch->n_requests, batch->n_traces, &a.w);
     CK(cudaMemsetAsync(ws, 0, ss::work_zero_bytes(batch->n_traces), st));
     int blocks = 0;

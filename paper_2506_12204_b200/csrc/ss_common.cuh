@@ -12,6 +12,12 @@ namespace ss {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr uint32_t ST_WAIT = 0, ST_DEC = 2, ST_DONE = 5, ST_UNS = 6;
 constexpr uint32_t F_STAGE = 7u, F_PF = 8u, F_Q = 16u, F_INS = 32u, F_FIRST = 64u, F_GRANT = 128u;
+// set with ST_UNS when the request was DECODING at _mark_unservable (engine.py:402-412 keeps its stage)
+constexpr uint32_t F_UDEC = 256u;
+// the per-request output state code: stage | prefilled << 8 | (unservable while decoding) << 9
+__host__ __device__ __forceinline__ uint32_t state_code(uint32_t flg) {
+    return (flg & F_STAGE) | ((flg & F_PF) ? 256u : 0u) | ((flg & F_UDEC) ? 512u : 0u);
+}
 constexpr uint32_t SLOT_MASK = 0x00FFFFFFu, DEC_BIT = 0x80000000u;
 
 struct __align__(16) Key {

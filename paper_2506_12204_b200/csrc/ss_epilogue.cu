@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(EPI_THREADS) epi_tiles_kernel(const __grid_con
             const Dyn d = DY[g];
             A.out.req.generated[g] = d.dec;
             if (A.out.req.f_t) A.out.req.f_t[g] = d.ft;
-            if (A.out.req.state) A.out.req.state[g] = (d.flg & F_STAGE) | ((d.flg & F_PF) ? 256u : 0u);
+            if (A.out.req.state) A.out.req.state[g] = state_code(d.flg);
             const double fi = A.out.req.finish_time[g];
             if (!isnan(fi)) {  // completed (metrics.py:24-32)
                 const double w = sub(fi, A.in.arrival_time[g]);

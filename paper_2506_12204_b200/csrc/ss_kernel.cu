@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     if (act) mem = sm->OM[lane];
                     // remaining_time of a decoding member (costs.py:174-191): reload(0)
                     // and prefill(0) are the same constants every round
-                    const double z0 = ss::add(reload_time(0, P), prefill_time(0, P));
+                    const double z0 = A.z0;  // a kernel-argument operand: no register held
                     constexpr bool sum_mode = sum_k;
                     constexpr unsigned long long DG = 0x9E3779B97F4A7C15ull, DG24 = DG << 24;
                     unsigned long long dgr = (unsigned long long)T.rounds * DG24;
@@ -1113,9 +1113,59 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             bool ok = true, pk = true;
                             double pft = 0.0;
                             uint32_t prk = 0, ptie = 0;
+                            // Order screen (lane i = member i). While no member's predicted
+                            // remainder clamps at 1 (costs.py:186-190), f_t of a decoding member
+                            // after j' more steps is T(m0 - j') with T(m) = g1*m*(C + 0.5 - 0.5m)
+                            // + g2*m exactly (C = prompt + mid): every member has the same
+                            // curvature -g1, so the real gap between two members is linear in
+                            // j' and its minimum over the chunk lies at an endpoint; f_t itself
+                            // is non-increasing (g1, g2 >= 0). The computed f_t of the first
+                            // and last round of the chunk bound every round's order: a gap
+                            // above 2^-40 f_t (>= 1000x the evaluation's rounding error)
+                            // at both ends keeps every pair in order at every round, and a
+                            // member 0 at least that far below the queue front keeps p*
+                            // ongoing. Same-rank members with equal (context, remainder)
+                            // evolve identically (their tie order stands). Otherwise the
+                            // exact per-round loop below decides.
+                            int i_lo = 0, i_hi = m - 1;  // members the exact loop evaluates
+#ifndef SS_NO_SCREEN
+                            if (A.screen) {
+                                const int l1 = (int)m_mid(mem) - (int)(mem.dec + (uint32_t)L);
+                                const uint32_t n0 = m_prompt(mem) + mem.dec + 1u;
+                                const int l0 = l1 + L - 1;
+                                const bool lin = l1 >= 1;
+                                const double f0 = ss::add(z0, decode_total_time_u32(n0, lin ? (uint32_t)l0 : 1u, P));
+                                const double f1 =
+                                    ss::add(z0, decode_total_time_u32(n0 + (uint32_t)(L - 1), lin ? (uint32_t)l1 : 1u, P));
+                                const double thr = 0x1p-40 * f0;
+                                const uint32_t rk = m_rank(mem);
+                                const double f0p = __shfl_up_sync(FULL, f0, 1), f1p = __shfl_up_sync(FULL, f1, 1);
+                                const uint32_t rkp = __shfl_up_sync(FULL, rk, 1), n0p = __shfl_up_sync(FULL, n0, 1);
+                                const int l0p = __shfl_up_sync(FULL, l0, 1);
+                                const bool linp = __shfl_up_sync(FULL, lin, 1);
+                                bool good;  // lane 0: p* stays ongoing; lane i: pair (i - 1, i) stays in order
+                                if (lane == 0) {
+                                    // member 0 against the queue front (kinf when empty)
+                                    const uint32_t frk = (uint32_t)(F0.hi >> 56);
+                                    const double fft = __longlong_as_double(
+                                        (long long)(((F0.hi & 0x00FFFFFFFFFFFFFFull) << 7) | (F0.lo >> 25)));
+                                    good = (F0.hi == ~0ull) | (rk < frk) | ((rk == frk) & lin & (fft - f0 > thr));
+                                } else {
+                                    good = (rkp < rk) | ((n0p == n0) & (l0p == l0)) |
+                                           (lin & linp & (f0 - f0p > thr) & (f1 - f1p > thr));
+                                }
+                                // only the pairs (and p*) the screen cannot settle run the exact loop
+                                const unsigned sus = __ballot_sync(FULL, act & !good);
+                                const int s_lo = __ffs(sus) - 1;
+                                i_lo = sus ? (s_lo > 0 ? s_lo - 1 : 0) : 1;
+                                i_hi = sus ? 31 - __clz(sus) : 0;
+                            }
+#endif
+                            SS_DCOUNT(6, i_hi < i_lo ? 1 : 0);
+                            SS_DCOUNT(7, i_hi >= i_lo ? i_hi - i_lo + 1 : 0);
                             // no warp-collective inside: a plain (unrollable) loop
 #pragma unroll kChunkUnroll
-                            for (int i = 0; i < m; i++) {
+                            for (int i = i_lo; i <= i_hi; i++) {
                                 const uint4 st = sm->OM[i].st;
                                 const uint32_t dec = sm->OM[i].dec + dj;
                                 int lft = (int)st.z - (int)dec;
@@ -1124,7 +1174,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                 const uint32_t rk = st.w >> 24, tie = st.w & SLOT_MASK;
                                 // key order (rank, f_t, tie) without packing: f_t > 0 orders like its bits
                                 if (i == 0) pk = klt_nb(make_key<POL>(rk, ft, tie, 0, true), F0);
-                                else ok &= (prk < rk) | ((prk == rk) & ((pft < ft) | ((pft == ft) & (ptie < tie))));
+                                else if (i > i_lo) ok &= (prk < rk) | ((prk == rk) & ((pft < ft) | ((pft == ft) & (ptie < tie))));
                                 pft = ft;
                                 prk = rk;
                                 ptie = tie;
@@ -1509,7 +1559,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                         A.w.R[T.off + ri] = last;
                                         A.w.rpos[T.off + last] = ri;
                                     }
-                                    flg_update(A, g, F_STAGE | F_Q | F_INS | F_GRANT, ST_UNS);
+                                    flg_update(A, g, F_STAGE | F_Q | F_INS | F_GRANT, ST_UNS | (isdec_k ? F_UDEC : 0u));
                                     A.out.unservable_slots[T.off + un] = mem.slot;
                                     c.nuns = un + 1;
                                 }
@@ -1923,7 +1973,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     const Dyn d = DYN(A)[g];
                     A.out.req.generated[g] = d.dec;
                     if (A.out.req.f_t) A.out.req.f_t[g] = d.ft;
-                    if (A.out.req.state) A.out.req.state[g] = (d.flg & F_STAGE) | ((d.flg & F_PF) ? 256u : 0u);
+                    if (A.out.req.state) A.out.req.state[g] = state_code(d.flg);
                     const double fi = A.out.req.finish_time[g];
                     if (!isnan(fi)) {
                         fin = true;

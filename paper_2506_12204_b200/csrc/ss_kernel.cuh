@@ -51,6 +51,8 @@ struct KArgs {
     ss_trace_batch in;
     ss_outputs out;
     Work w;
+    double z0;  // reload(0) + prefill(0) of a decoding request's remaining time (costs.py:174-191), host-computed
+    int screen; // the chunk's order screen is valid: gamma1, gamma2 >= 0 and finite, z0 == 0 (ss_kernel.cu)
 };
 
 constexpr int PP_THREADS = 256;               // prepass CTA size

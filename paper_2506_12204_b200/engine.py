@@ -201,6 +201,13 @@ class Simulator:
             r.prefilled_tokens = r.prompt_len if pf else 0
             if stg in _STAGE_BACK:
                 r.stage = _STAGE_BACK[stg]
+            elif stg == A.SS_STAGE_UNSERVABLE:
+                # _mark_unservable (engine.py:402-412) keeps the stage and the host KV and
+                # releases the device KV; bit 9 says the request was DECODING then
+                r.stage = Stage.DECODING if (code >> 9) & 1 else Stage.WAITING
+                r.kv_device_tokens = 0
+                r.kv_host_tokens = 0 if r.stage is Stage.DECODING else r.prefilled_tokens + r.decoded_tokens
+                continue
             if r.stage is Stage.DECODING:
                 r.kv_device_tokens, r.kv_host_tokens = r.prefilled_tokens + r.decoded_tokens, 0
             elif r.stage is Stage.WAITING:

@@ -186,6 +186,9 @@ def test_run_dropin_matches_golden(native):
             assert rec.generated_tokens == want[3] and rec.evictions == want[4]
         ends = [e for e in tr.events if e.kind is EventKind.ITERATION_END]
         assert len(ends) == len(exp["log"])
+        # the caller's Request objects end in the reference's final stage (runtime
+        # unservable requests keep the stage they had when marked, engine.py:402-412)
+        assert [r.stage.value for r in arrivals] == exp["final_stage"], case["name"]
 
 
 # ---- bulk admission: grid-wide radix sort + sorted RUN (ss_prepass.cu) ------
@@ -375,3 +378,26 @@ def test_gpu_pipelined_host_call_vs_oracle(native, capacity):
     if logs:
         for t in range(0, batch.n_traces, 97):
             assert np.array_equal(gpu.logs[t], cpu.logs[t]), t
+
+
+@variants
+def test_gpu_unservable_duplicate_pinned(native, variant):
+    """The one documented divergence ("Not emulated"): seed
+    2808, 40 requests, b = 8, 400 slots. A request marked unservable mid-round
+    keeps a stale duplicate copy in the same batch that the reference keeps
+    decoding; the oracle follows the reference into its IllegalTransitionError
+    (REF_ERROR), the kernel stops the trace as LIVELOCK. Both report the same
+    round count. Pinned so that a change on either side shows up."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.results import make_params
+    from paper_2506_12204_b200.tracegen import generate_batch
+    from paper_2506_12204_b200.workload import WorkloadSpec
+
+    batch = generate_batch(WorkloadSpec(total_requests=40, levels=3), [2808], pinned=False)
+    p = lambda: make_params(get_profile("a100_qwen7b"), 8, 400, levels=3, flags=A.SS_FLAG_DIGEST | VARIANTS[variant])
+    gpu = native.run_host(p(), batch)
+    cpu = run_oracle(p(), batch)
+    assert int(cpu.stats["status"][0]) == A.SS_TRACE_REF_ERROR
+    assert int(gpu.stats["status"][0]) == A.SS_TRACE_LIVELOCK
+    assert int(gpu.stats["rounds"][0]) == int(cpu.stats["rounds"][0])

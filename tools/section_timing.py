@@ -31,6 +31,6 @@ c = v[16:]
 print(f"  chunks {c[0]}, chunk rounds {c[1]} ({c[1] / max(c[0], 1):.1f}/chunk), per-round fast {c[2]}, general {c[3]}")
 if c[5]: print(f"  refills {c[5]}, cycles per refill {v[15] / c[5]:.0f}")
 if c[4]: print(f"  evict_one calls {c[4]}, cycles per call {v[14] / c[4]:.0f}")
-if c[0]: print(f"  cycles/chunk {v[2] / c[0]:.0f}, per chunk round {v[2] / max(c[1], 1):.0f}")
+if c[0]: print(f"  cycles/chunk {v[2] / c[0]:.0f}, per chunk round {v[2] / max(c[1], 1):.0f}, order screen settled {100 * c[6] / c[0]:.1f}% of chunks, exact loop {c[7] / c[0]:.2f} members per chunk")
 if c[2]: print(f"  cycles per per-round fast round {v[1] / c[2]:.0f}")
 if c[3]: print(f"  cycles per general round (composition .. queue rebuild) {sum(v[i] for i in (3, 8, 9, 10, 11, 12, 13)) / c[3]:.0f}")
