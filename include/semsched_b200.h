@@ -114,7 +114,8 @@ typedef struct ss_params {
                                   per-request outputs and waiting-time sums
                                   (metrics.py:35-56) to two grid-wide kernels
                                   (exact double-double tile sums, 1e-15 relative to
-                                  CPython's sum) instead of its scheduler warp
+                                  CPython's sum); every shorter trace is finished
+                                  by one warp of the short-trace epilogue kernel
                                   (sequential CPython sum, bit-exact).
                                   0 = SS_EPILOGUE_MIN_DEFAULT, < 0 = never.      */
 } ss_params;

@@ -3,8 +3,7 @@
 // When a trace ends (engine.py:226-243) its per-request records are read out
 // (RequestRecord generated tokens, final f_t / stage) and the waiting-time
 // statistics are reduced (metrics.py:35-56: average wait, per-level and overall
-// normalized wait, over completed records). A short trace does that in its own
-// scheduler warp (ss_kernel.cu, CPython's sequential sum reproduced bit for bit).
+// normalized wait, over completed records), after the scheduler kernels.
 // For a long trace — config C's single pool of 1,000,000 requests — one warp
 // would stream every record alone (26 ms), so traces of >= epilogue_min
 // requests are finished here by the whole grid after the scheduler kernels:
@@ -19,6 +18,13 @@
 // The result is the correctly rounded sum except within ~1e-30 of a rounding
 // tie; CPython's Neumaier sum is compensated too, so the two agree to ~1 ulp
 // (tests: 1e-12 relative, north_star's contract is 1e-6).
+//
+// Every other trace is finished by epi_short_kernel, one warp per trace, after
+// the scheduler kernels: coalesced record read-out 32 requests at a time and
+// CPython 3.12's sequential float sum (Neumaier) in record order, bit for bit
+// (lane 31: waits, lane 30: normalized waits, lane l < 16: level l). Thousands
+// of such warps overlap their dependent sum chains; inside the scheduler the
+// same work sat on each trace's serial critical path.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -92,7 +98,7 @@ __global__ void __launch_bounds__(EPI_THREADS) epi_tiles_kernel(const __grid_con
 #pragma unroll
         for (int c = 0; c <= SS_MAX_LEVELS; c++) cnt[c] = 0;
         for (long long i = i0 + threadIdx.x; i < i1; i += EPI_THREADS) {
-            // RequestRecord read-out, as the scheduler warp does for short traces
+            // RequestRecord read-out, as epi_short_kernel does for short traces
             const long long g = off + i;
             const Dyn d = DY[g];
             A.out.req.generated[g] = d.dec;
@@ -180,11 +186,74 @@ __global__ void __launch_bounds__(EPI_THREADS) epi_final_kernel(const __grid_con
     }
 }
 
+constexpr int EPS_THREADS = 256;
+
+// one warp per short trace (epT[t] == 0): RequestRecord read-out and the exact
+// CPython-3.12 sums (metrics.py:35-56) in record order
+__global__ void __launch_bounds__(EPS_THREADS) epi_short_kernel(const __grid_constant__ KArgs A) {
+    const int T = A.in.n_traces;
+    const int t = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= T || A.w.epT[t] != 0) return;
+    const Dyn* DY = reinterpret_cast<const Dyn*>(A.w.dy);
+    const long long off = A.in.trace_offsets[t];
+    const int n = (int)(A.in.trace_offsets[t + 1] - off);
+    PySum acc;
+    acc.init();
+    for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        double w = 0.0, nw = 0.0;
+        bool fin = false;
+        int lv = 0;
+        if (i < n) {
+            const long long g = off + i;
+            const Dyn d = DY[g];
+            A.out.req.generated[g] = d.dec;
+            if (A.out.req.f_t) A.out.req.f_t[g] = d.ft;
+            if (A.out.req.state) A.out.req.state[g] = state_code(d.flg);
+            const double fi = A.out.req.finish_time[g];
+            if (!isnan(fi)) {  // completed (metrics.py:24-32)
+                fin = true;
+                w = sub(fi, A.in.arrival_time[g]);
+                nw = dv(w, (double)d.dec);
+                lv = A.in.true_urgency[g];
+            }
+        }
+        unsigned fm = __ballot_sync(FULL, fin);
+        while (fm) {
+            const int k = __ffs(fm) - 1;
+            fm &= fm - 1;
+            const double wk = __shfl_sync(FULL, w, k), nk = __shfl_sync(FULL, nw, k);
+            const int lk = __shfl_sync(FULL, lv, k);
+            if (lane == 31) acc.push(wk);
+            else if (lane == 30) acc.push(nk);
+            else if (lane == lk && lane < SS_MAX_LEVELS) acc.push(nk);
+        }
+    }
+    const double val = acc.value();
+    ss_trace_stats* st = A.out.stats + t;
+    if (lane < SS_MAX_LEVELS) {
+        st->level_norm_sum[lane] = val;
+        st->level_count[lane] = acc.n;
+    }
+    if (lane == 30) st->sum_norm_wait = val;
+    if (lane == 31) {
+        st->sum_wait = val;
+        st->completed = acc.n;
+    }
+}
+
 }  // namespace
 
 int launch_epilogue(const KArgs& a, void* stream) {
-    if (epilogue_threshold(a.P) <= 0 || a.in.n_traces == 0 || a.in.n_requests == 0) return SS_OK;
+    if (a.in.n_traces == 0) return SS_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    {
+        const long long threads = (long long)a.in.n_traces * 32;
+        epi_short_kernel<<<(int)((threads + EPS_THREADS - 1) / EPS_THREADS), EPS_THREADS, 0, st>>>(a);
+        if (cudaGetLastError() != cudaSuccess) return SS_ERR_CUDA;
+    }
+    if (epilogue_threshold(a.P) <= 0 || a.in.n_requests == 0) return SS_OK;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

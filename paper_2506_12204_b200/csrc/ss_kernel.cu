@@ -1955,60 +1955,12 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             T.nins = 0;
         }
 
-        // ---- outputs and the fused statistics (metrics.py:35-56); a long trace
-        // (config C's 1M pool) leaves both to the grid-wide epilogue (ss_epilogue.cu)
+        // ---- per-trace results; the per-request outputs and the fused waiting-time
+        // statistics (metrics.py:35-56) are finished after this kernel by ss_epilogue.cu
         SS_SECT(4);
         {
-            const long long epi_min = epilogue_threshold(A.P);
-            const bool warp_end = !(epi_min > 0 && (long long)n >= epi_min);
-            PySum acc;
-            acc.init();
-            for (int base = 0; uni(warp_end && base < n); base += 32) {
-                const int i = base + lane;
-                double w = 0.0, nw = 0.0;
-                bool fin = false;
-                int lv = 0;
-                if (i < n) {
-                    const long long g = T.off + i;
-                    const Dyn d = DYN(A)[g];
-                    A.out.req.generated[g] = d.dec;
-                    if (A.out.req.f_t) A.out.req.f_t[g] = d.ft;
-                    if (A.out.req.state) A.out.req.state[g] = state_code(d.flg);
-                    const double fi = A.out.req.finish_time[g];
-                    if (!isnan(fi)) {
-                        fin = true;
-                        w = ss::sub(fi, A.in.arrival_time[g]);
-                        nw = ss::dv(w, (double)d.dec);
-                        lv = A.in.true_urgency[g];
-                    }
-                }
-                unsigned fm = __ballot_sync(FULL, fin);
-                while (fm) {
-                    const int k = __ffs(fm) - 1;
-                    fm &= fm - 1;
-                    const double wk = __shfl_sync(FULL, w, k), nk = __shfl_sync(FULL, nw, k);
-                    const int lk = __shfl_sync(FULL, lv, k);
-                    if (lane == 31) acc.push(wk);
-                    else if (lane == 30) acc.push(nk);
-                    else if (lane == lk && lane < SS_MAX_LEVELS) acc.push(nk);
-                }
-            }
             dig = warp_sum_u64(dig);
-            const double val = acc.value();
-            const int cntv = acc.n;
-            __syncwarp();
             ss_trace_stats* st = A.out.stats + t;
-            if (warp_end) {
-                if (lane < SS_MAX_LEVELS) {
-                    st->level_norm_sum[lane] = val;
-                    st->level_count[lane] = cntv;
-                }
-                if (lane == 30) st->sum_norm_wait = val;
-                if (lane == 31) {
-                    st->sum_wait = val;
-                    st->completed = cntv;
-                }
-            }
             if (lane == 0) {
                 st->digest = want_digest ? dig : 0ull;
                 st->rounds = T.rounds;

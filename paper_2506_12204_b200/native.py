@@ -64,10 +64,10 @@ EXPORTED = ("ss_last_error", "ss_device_info", "ss_workspace_bytes", "ss_run_tra
             "ss_audit_last_kernel_ms", "ss_generate_traces", "ss_generate_traces_device")
 
 
-# kernels one ss_run_traces call launches (ss_prepass.cu + the scheduler):
-# detect, eoff scan, init, bulk keys, histogram, plan, 16 x (count, scan,
-# scatter), final copy, sched_kernel. The bulk stages exit at once when no
-# trace admits a bulk group.
+# kernels one ss_run_traces call launches (ss_prepass.cu + the scheduler +
+# ss_epilogue.cu): detect, eoff scan, init, bulk keys, histogram, plan,
+# 16 x (count, scan, scatter), final copy, sched_kernel, the end-of-trace
+# kernels. The bulk stages exit at once when no trace admits a bulk group.
 def launches_per_run(params=None, max_trace_len=None) -> int:
     bulk = params is None or params.bulk_min >= 0
     if params is not None and max_trace_len is not None:
@@ -76,7 +76,9 @@ def launches_per_run(params=None, max_trace_len=None) -> int:
     # launch the three variants (chunked without eviction, chunked, per-round); the
     # unselected ones exit at once
     sched = 3 if params is None or params.policy == A.SS_POLICY["semantic"] else 1
-    epi = 2 if params is None or _epilogue_possible(params, max_trace_len) else 0
+    # the short-trace epilogue (outputs + exact sums, one warp per trace) always runs;
+    # the two grid-wide long-trace kernels only when a trace is long enough
+    epi = 1 + (2 if params is None or _epilogue_possible(params, max_trace_len) else 0)
     return 4 + (3 + 16 * 3 + 1 if bulk else 0) + sched + epi
 
 

@@ -18,12 +18,13 @@ from collections import defaultdict
 
 # kernel line ranges (ss_kernel.cu) -> section name; edit to the file's layout
 SECTIONS = [
-    ("trace init", 659, 772), ("admission/refill/anom", 773, 844), ("stretch entry+setup", 845, 935),
-    ("per-round fast body", 936, 1067), ("chunk", 1068, 1174), ("stretch order/exit", 1175, 1218),
-    ("g: composition", 1219, 1409), ("g: KV admission (excl. evict)", 1410, 1540),
-    ("g: nothing granted", 1541, 1572), ("g: batch duration", 1573, 1613), ("g: progress", 1614, 1765),
-    ("g: record+digest", 1766, 1818), ("g: ongoing rebuild", 1819, 1854), ("g: queue rebuild", 1855, 1883),
-    ("outputs/stats", 1884, 1970),
+    ("trace init", 659, 772), ("admission/refill/anom", 773, 848), ("stretch entry+setup+vote", 849, 960),
+    ("per-round fast body", 961, 1090), ("chunk: clock chain", 1091, 1129), ("chunk: order screen", 1130, 1166),
+    ("chunk: exact loop", 1167, 1184), ("chunk: stop vote", 1185, 1195), ("chunk: digest", 1196, 1209),
+    ("chunk: log", 1210, 1228), ("chunk: commit", 1229, 1247), ("stretch order/exit", 1248, 1292),
+    ("g: composition", 1293, 1482), ("g: KV admission", 1483, 1647), ("g: batch duration", 1648, 1688),
+    ("g: progress", 1689, 1839), ("g: record+digest", 1840, 1892), ("g: ongoing rebuild", 1893, 1934),
+    ("g: queue rebuild", 1935, 1957), ("outputs/stats", 1958, 2041),
 ]
 
 

@@ -12,7 +12,8 @@ W = sys.argv[1]
 wl = bench.WORKLOADS[W]
 T = int(sys.argv[2]) if len(sys.argv) > 2 else wl["traces"]
 batch = bench.native_batch(W, wl, np.arange(T), pinned=False)
-prm = make_params(get_profile(wl["profile"]), 16, wl["capacity"], levels=wl["levels"], flags=A.SS_FLAG_DIGEST)
+force = {"auto": 0, "chunked": A.SS_FLAG_FORCE_CHUNKED, "perround": A.SS_FLAG_FORCE_PERROUND}[os.environ.get("SS_BENCH_VARIANT", "auto")]
+prm = make_params(get_profile(wl["profile"]), 16, wl["capacity"], levels=wl["levels"], flags=A.SS_FLAG_DIGEST | force)
 lib = native.lib()
 buf = (C.c_ulonglong * 24)()
 native.run_host(prm, batch)  # warm-up
