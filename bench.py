@@ -231,8 +231,9 @@ def params_for(wl, flags=None):
     from paper_2506_12204_b200.results import make_params
 
     force = {"auto": 0, "chunked": A.SS_FLAG_FORCE_CHUNKED, "perround": A.SS_FLAG_FORCE_PERROUND}[VARIANT]
+    dflt = 0 if os.environ.get("SS_BENCH_NODIGEST") else A.SS_FLAG_DIGEST  # dev: cost of the digest
     return make_params(get_profile(wl["profile"]), 16, wl["capacity"], levels=wl["levels"],
-                       flags=(A.SS_FLAG_DIGEST if flags is None else flags) | force)
+                       flags=(dflt if flags is None else flags) | force)
 
 
 # ------------------------------------------------------------- CPU legs -----

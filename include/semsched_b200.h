@@ -217,8 +217,9 @@ typedef struct ss_outputs {
  * The granted list of round r contributes
  *     ss_round_mul(r) * sum_pos ss_grant_term(pos, slot_pos)      (mod 2^64)
  * (an odd round multiplier times a position-tagged hash of the list), so a
- * batch that stays the same over a stretch of rounds hashes once; every other
- * field is one ss_term(round, tag, index, value). */
+ * batch that stays the same over a stretch of rounds hashes once; the header,
+ * memory and time fields are ss_round_fields(round, ...) below; every other
+ * field (completions, eviction decisions) is one ss_term(round, tag, index, value). */
 #if defined(__CUDACC__)
 #define SS_HD __host__ __device__ __forceinline__
 #else
@@ -239,9 +240,26 @@ SS_HD uint64_t ss_grant_term(uint32_t pos, uint64_t slot) {
     return ss_mix64(slot ^ ((uint64_t)(pos + 1u) * SS_DG_POS));
 }
 SS_HD uint64_t ss_round_mul(uint64_t round) { return (2u * round + 1u) * SS_DG_ROUND; }
-#define SS_TAG_HDR   1u
-#define SS_TAG_MEM   2u
-#define SS_TAG_TIME  3u
+/* The three fields every round has (header word, KV slots in use, round end
+ * time bits) enter as one weighted sum, linear in each field:
+ *     ss_round_fields(r, hdr, mem, t) =
+ *         (2r+1) * (K_H (hdr ^ S_H) + K_M (mem ^ S_M) + K_T (t ^ S_T))   (mod 2^64)
+ * With odd weights a change of any one field changes the digest, and a round's
+ * fields cost three multiply-adds instead of three 64-bit mixes (in the kernel's
+ * stretches of same-batch rounds this was a third of the scheduler's time). */
+#define SS_DG_HDR  0xD1B54A32D192ED03ull
+#define SS_DG_MEM  0xAEF17502108EF2D9ull
+#define SS_DG_TIME 0xF1357AEA2E62A9C5ull
+#define SS_DS_HDR  0x5851F42D4C957F2Dull
+#define SS_DS_MEM  0x14057B7EF767814Full
+#define SS_DS_TIME 0x2545F4914F6CDD1Dull
+SS_HD uint64_t ss_round_fields(uint64_t round, uint64_t hdr, uint64_t mem, uint64_t tbits) {
+    return (2u * round + 1u) *
+           (SS_DG_HDR * (hdr ^ SS_DS_HDR) + SS_DG_MEM * (mem ^ SS_DS_MEM) + SS_DG_TIME * (tbits ^ SS_DS_TIME));
+}
+#define SS_TAG_HDR   1u   /* unused since ss_round_fields */
+#define SS_TAG_MEM   2u   /* unused since ss_round_fields */
+#define SS_TAG_TIME  3u   /* unused since ss_round_fields */
 #define SS_TAG_GRANT 4u   /* unused since the grant terms above */
 #define SS_TAG_DONE  5u
 #define SS_TAG_EV0   6u   /* victim | action<<32     */

@@ -457,10 +457,8 @@ static void record_round(osim* s, int kind, const int* g, int m, const int* c, i
     int v = s->ndec;
     uint64_t r = (uint64_t)s->rounds;
     if (s->P->flags & SS_FLAG_DIGEST) {
-        uint64_t d = ss_term(r, SS_TAG_HDR, 0, ss_hdr_word(kind, m, nc, v));
-        d += ss_term(r, SS_TAG_MEM, 0, (uint64_t)s->used);
         uint64_t tb; memcpy(&tb, &t, 8);
-        d += ss_term(r, SS_TAG_TIME, 0, tb);
+        uint64_t d = ss_round_fields(r, ss_hdr_word(kind, m, nc, v), (uint64_t)s->used, tb);
         uint64_t gh = 0;
         for (int j = 0; j < m; j++) gh += ss_grant_term((uint32_t)j, (uint64_t)g[j]);
         d += gh * ss_round_mul(r);

@@ -860,18 +860,13 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     // and prefill(0) are the same constants every round
                     const double z0 = A.z0;  // a kernel-argument operand: no register held
                     constexpr bool sum_mode = sum_k;
-                    constexpr unsigned long long DG = 0x9E3779B97F4A7C15ull, DG24 = DG << 24;
-                    unsigned long long dgr = (unsigned long long)T.rounds * DG24;
                     // per-membership values, recomputed when members complete
                     int left;                 // rounds before the first completion (dec + 1 >= tout)
                     unsigned nmax;            // longest context + 1 (decode step of the batch)
                     long long safe_used;      // per-round kernels: no member evicts while used <= this
                     int evleft;               // chunked kernels: rounds before the first one that evicts
                     unsigned long long gt;    // this lane's grant term (ss_grant_term of its batch position)
-                    unsigned long long hb;    // chunked kernels: the batch list's hash (sum of the grant terms)
-                    // header lanes 29..31: tag pre-multiplied (ss_term); round multiplier of the grant terms
-                    const unsigned long long dgc =
-                        ((unsigned long long)(lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME)) << 20) * DG;
+                    // round multiplier of the grant terms
                     unsigned long long rmul = ss_round_mul((unsigned long long)T.rounds);
                     auto setup = [&]() {
                         left = __reduce_min_sync(FULL, act ? (int)(m_tout(mem) - mem.dec) - 1 : 0x7fffffff);
@@ -905,7 +900,6 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             evleft = __reduce_min_sync(FULL, act ? safe : 0x7fffffff);
                         }
                         gt = act ? ss_grant_term((uint32_t)lane, mem.slot) : 0ull;
-                        if (chunking) hb = warp_sum_u64(gt);
                     };
                     // chunked kernels: one call site (one copy of its code) at the loop top;
                     // per-round kernels call it directly (no extra vote per round)
@@ -999,32 +993,22 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         const int ncd = __popc(cdm);
                         if (want_digest) {
                             const unsigned long long r64 = (unsigned long long)T.rounds;
-                            const bool hl = lane >= 29;
-                            // header / memory / time terms in lanes 29..31 (branch-free role select);
-                            // the members' cached grant terms times this round's multiplier
-                            const unsigned long long hv = ss_hdr_word(SS_KIND_DECODE, m, ncd, 0);
-                            const unsigned long long mv = (unsigned long long)T.used, tv = dbits(end);
-                            unsigned long long val = (lane == 30) ? mv : tv;
-                            val = (lane == 31) ? hv : val;
-                            // ss_term(r, tag, 0, val) with ((r << 24) ^ c) * G = r * (G << 24) + c * G
-                            // (c < 2^24): the round part advances by one add per round
-                            // completion terms share the hash pass with the header lanes; a
-                            // completing header lane (b > 29) takes a second pass
-                            const bool dn = (cdm >> lane) & 1u;
-                            const unsigned long long dx =
-                                (unsigned long long)mem.slot ^
-                                (((r64 << 24) ^ ((unsigned long long)SS_TAG_DONE << 20) ^ (unsigned long long)__popc(cdm & lt)) *
-                                 0x9E3779B97F4A7C15ull);
+                            // the members' cached grant terms times this round's multiplier; the
+                            // completion terms (completion rounds only); header / memory / time as
+                            // one weighted sum (ss_round_fields) in lane 31
                             dig += act ? gt * rmul : 0ull;
-                            const int passes = 1 + (__any_sync(FULL, dn && hl) ? 1 : 0);
-#pragma unroll 1
-                            for (int ps = 0; ps < passes; ps++) {
-                                const bool hdr = ps == 0 && hl, use = hdr || (dn && (ps == 1) == hl);
-                                const unsigned long long term = ss_mix64(hdr ? (val ^ (dgr + dgc)) : dx);
-                                dig += use ? term : 0ull;
+                            if (cround) {
+                                const bool dn = (cdm >> lane) & 1u;
+                                const unsigned long long dx =
+                                    (unsigned long long)mem.slot ^
+                                    (((r64 << 24) ^ ((unsigned long long)SS_TAG_DONE << 20) ^ (unsigned long long)__popc(cdm & lt)) *
+                                     0x9E3779B97F4A7C15ull);
+                                dig += dn ? ss_mix64(dx) : 0ull;
                             }
+                            if (lane == 31)
+                                dig += ss_round_fields(r64, ss_hdr_word(SS_KIND_DECODE, m, ncd, 0), (unsigned long long)T.used,
+                                                       dbits(end));
                         }
-                        dgr += DG24;
                         rmul += 2u * SS_DG_ROUND;
                         if (logging) {
                             const long long lp = c.logpos;
@@ -1194,18 +1178,15 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             const bool runj = lane < Lx;
                             const long long used_j = T.used + (long long)(lane + 1) * m;
                             if (want_digest) {
-                                const unsigned long long hv = ss_hdr_word(SS_KIND_DECODE, m, 0, 0);
-                                // header / memory / time terms through one copy of the hash (code
-                                // size: three inlined copies measured 3% slower)
-                                unsigned long long tr = 0ull;
-#pragma unroll 1
-                                for (int f = 0; f < 3; f++) {
-                                    const unsigned long long val = f == 0 ? hv : (f == 1 ? (unsigned long long)used_j : dbits(endj));
-                                    tr += ss_term(rj, f == 0 ? SS_TAG_HDR : (f == 1 ? SS_TAG_MEM : SS_TAG_TIME), 0, val);
-                                }
-                                // the batch list hashes once: sum of the members' grant terms
-                                // hb: the batch list's hash, summed once per membership (setup)
-                                dig += runj ? hb * ss_round_mul(rj) + tr : 0ull;
+                                // ss_round_fields of round j (the header is constant over the chunk);
+                                // the grant terms of rounds r0..r0+Lx-1: each member's term times
+                                // sum_j ss_round_mul(r0 + j) = SS_DG_ROUND * Lx * (2 r0 + Lx)
+                                const unsigned long long cst = SS_DG_HDR * (ss_hdr_word(SS_KIND_DECODE, m, 0, 0) ^ SS_DS_HDR);
+                                const unsigned long long v = cst + SS_DG_MEM * ((unsigned long long)used_j ^ SS_DS_MEM) +
+                                                             SS_DG_TIME * (dbits(endj) ^ SS_DS_TIME);
+                                const unsigned long long gsum =
+                                    SS_DG_ROUND * ((unsigned long long)Lx * (2ull * (unsigned long long)T.rounds + (unsigned long long)Lx));
+                                dig += (runj ? (2ull * rj + 1ull) * v : 0ull) + (act ? gt * gsum : 0ull);
                             }
                             if (logging) {
                                 __syncwarp();
@@ -1237,7 +1218,6 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             k += Lx;
                             spool += (long long)Lx * live_s;
                             sgr += (long long)Lx * m;
-                            dgr += (unsigned long long)Lx * DG24;
                             rmul += (unsigned long long)Lx * (2u * SS_DG_ROUND);
                             mem.dec += (uint32_t)Lx;
                             long long lft = (long long)m_mid(mem) - (long long)mem.dec;
@@ -1620,11 +1600,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             if (uni(ng == 0)) {
                 // nothing granted (engine.py:329-344): clock does not advance
                 T.nO = 0;
-                if (want_digest && lane < 3) {  // header / memory / time, one lane each
-                    const unsigned long long val = lane == 0 ? ss_hdr_word(SS_KIND_NONE, 0, 0, R.ndec)
-                                                             : (lane == 1 ? (unsigned long long)T.used : dbits(T.clock));
-                    dig += ss_term(r64, lane == 0 ? SS_TAG_HDR : (lane == 1 ? SS_TAG_MEM : SS_TAG_TIME), 0, val);
-                }
+                if (want_digest && lane == 0)  // header / memory / time
+                    dig += ss_round_fields(r64, ss_hdr_word(SS_KIND_NONE, 0, 0, R.ndec), (unsigned long long)T.used,
+                                           dbits(T.clock));
                 if (R.ndec > 0 && lane == 0) {
                     if (T.used > peak) peak = T.used;
                     if (logging && c.log) {
@@ -1842,30 +1820,24 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 const int nc_done = __popc(cdone);
                 const int gi = __popc(R.G & lt), ci = __popc(cdone & lt);
                 if (want_digest) {
-                    // one hash stream: granted lanes hash their slot, lanes 29..31
-                    // the round header (a second pass only when they are granted)
-                    const bool hl = lane >= 29;
-                    const uint32_t htag = lane == 31 ? SS_TAG_HDR : (lane == 30 ? SS_TAG_MEM : SS_TAG_TIME);
-                    const unsigned long long hval =
-                        lane == 31 ? ss_hdr_word(kind, ng, nc_done, R.ndec)
-                                   : (lane == 30 ? (unsigned long long)T.used : dbits(end));
-                    // up to three passes through one copy of the hash: 0 grant term (granted
-                    // lanes) or header term (lanes 29..31); 1 header term of granted lanes
-                    // 29..31 (b > 29); 2 completion terms
-                    const unsigned long long hsalt = ((r64 << 24) ^ ((unsigned long long)htag << 20)) * 0x9E3779B97F4A7C15ull;
+                    // one hash stream: granted lanes hash their slot (pass 0), completing lanes
+                    // their completion term (pass 1); header / memory / time as one weighted
+                    // sum (ss_round_fields) in lane 31
                     const unsigned long long dsalt = ((r64 << 24) ^ ((unsigned long long)SS_TAG_DONE << 20) ^
                                                       (unsigned long long)ci) * 0x9E3779B97F4A7C15ull;
 #pragma unroll 1
-                    for (int ps = 0; ps < 3; ps++) {
-                        const bool use = ps == 0 ? (g_act || hl) : (ps == 1 ? (m > 29 && hl && g_act) : (done && cdone != 0));
+                    for (int ps = 0; ps < 2; ps++) {
+                        const bool use = ps == 0 ? g_act : (done && cdone != 0);
                         if (!__any_sync(FULL, use)) continue;
-                        const bool grant = ps == 0 && g_act;
                         const unsigned long long x =
-                            grant ? ((unsigned long long)mem.slot ^ ((unsigned long long)(gi + 1) * SS_DG_POS))
-                                  : (ps == 2 ? ((unsigned long long)mem.slot ^ dsalt) : (hval ^ hsalt));
+                            ps == 0 ? ((unsigned long long)mem.slot ^ ((unsigned long long)(gi + 1) * SS_DG_POS))
+                                    : ((unsigned long long)mem.slot ^ dsalt);
                         const unsigned long long h = ss_mix64(x);
-                        dig += use ? (grant ? h * ss_round_mul(r64) : h) : 0ull;
+                        dig += use ? (ps == 0 ? h * ss_round_mul(r64) : h) : 0ull;
                     }
+                    if (lane == 31)
+                        dig += ss_round_fields(r64, ss_hdr_word(kind, ng, nc_done, R.ndec), (unsigned long long)T.used,
+                                               dbits(end));
                 }
                 if (logging) {
                     const long long lp = c.logpos;

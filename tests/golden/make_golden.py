@@ -65,6 +65,13 @@ def round_mul(rnd):
     return ((2 * rnd + 1) * 0xA0761D6478BD642F) & M64
 
 
+def round_fields(rnd, hdr, mem, tbits):
+    # include/semsched_b200.h ss_round_fields
+    v = (0xD1B54A32D192ED03 * (hdr ^ 0x5851F42D4C957F2D) + 0xAEF17502108EF2D9 * (mem ^ 0x14057B7EF767814F)
+         + 0xF1357AEA2E62A9C5 * (tbits ^ 0x2545F4914F6CDD1D))
+    return ((2 * rnd + 1) * v) & M64
+
+
 def fbits(x):
     return struct.unpack("<Q", struct.pack("<d", x))[0]
 
@@ -202,9 +209,8 @@ def run_case(name, cfg, arrivals_fn, keep_log):
         g = [slot[i] for i in rd["granted"]]
         c = [slot[i] for i in rd["completed"]]
         decs = rd["decisions"]
-        d = term(k, 1, 0, rd["kind"] | (len(g) << 8) | (len(c) << 24) | (len(decs) << 40))
-        d += term(k, 2, 0, rd["mem_used"])
-        d += term(k, 3, 0, fbits(rd["time"]))
+        d = round_fields(k, rd["kind"] | (len(g) << 8) | (len(c) << 24) | (len(decs) << 40), rd["mem_used"],
+                         fbits(rd["time"]))
         gh = 0
         for j, s in enumerate(g):
             gh += grant_term(j, s)
