@@ -18,13 +18,13 @@ from collections import defaultdict
 
 # kernel line ranges (ss_kernel.cu) -> section name; edit to the file's layout
 SECTIONS = [
-    ("trace init", 659, 772), ("admission/refill/anom", 773, 848), ("stretch entry+setup+vote", 849, 960),
-    ("per-round fast body", 961, 1090), ("chunk: clock chain", 1091, 1129), ("chunk: order screen", 1130, 1166),
-    ("chunk: exact loop", 1167, 1184), ("chunk: stop vote", 1185, 1195), ("chunk: digest", 1196, 1209),
-    ("chunk: log", 1210, 1228), ("chunk: commit", 1229, 1247), ("stretch order/exit", 1248, 1292),
-    ("g: composition", 1293, 1482), ("g: KV admission", 1483, 1647), ("g: batch duration", 1648, 1688),
-    ("g: progress", 1689, 1839), ("g: record+digest", 1840, 1892), ("g: ongoing rebuild", 1893, 1934),
-    ("g: queue rebuild", 1935, 1957), ("outputs/stats", 1958, 2041),
+    ("trace init", 659, 772), ("admission/refill/anom", 773, 848), ("stretch entry+setup+vote", 849, 954),
+    ("per-round fast body", 955, 1074), ("chunk: clock chain", 1075, 1113), ("chunk: order screen", 1114, 1150),
+    ("chunk: exact loop", 1151, 1168), ("chunk: stop vote", 1169, 1179), ("chunk: digest", 1180, 1191),
+    ("chunk: log", 1192, 1209), ("chunk: commit", 1210, 1227), ("stretch order/exit", 1228, 1272),
+    ("g: composition", 1273, 1462), ("g: KV admission", 1463, 1625), ("g: batch duration", 1626, 1666),
+    ("g: progress", 1667, 1817), ("g: record+digest", 1818, 1864), ("g: ongoing rebuild", 1865, 1906),
+    ("g: queue rebuild", 1907, 1931), ("outputs/stats", 1932, 1965),
 ]
 
 
