@@ -319,6 +319,9 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
     // work queued on the slice streams, which must drain before the staging
     // buffers (and the g_stage lock) are given up
     auto run_slices = [&]() -> int {
+        // the round log is copied back whole: its words past each trace's log_words
+        // are defined (zero) rather than left over from earlier calls (initcheck)
+        if (logr) CK(cudaMemsetAsync(dout.round_log, 0, (size_t)log_words * 4, cs));
         CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CK(cudaEventRecord(ev_in, cs));
         if (kernel_ms && S > 1) {
