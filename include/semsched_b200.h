@@ -218,8 +218,9 @@ typedef struct ss_outputs {
  *     ss_round_mul(r) * sum_pos ss_grant_term(pos, slot_pos)      (mod 2^64)
  * (an odd round multiplier times a position-tagged hash of the list), so a
  * batch that stays the same over a stretch of rounds hashes once; the header,
- * memory and time fields are ss_round_fields(round, ...) below; every other
- * field (completions, eviction decisions) is one ss_term(round, tag, index, value). */
+ * memory and time fields are ss_round_fields(round, ...) below; a completion is
+ * one ss_term(round, SS_TAG_DONE, index, slot), an eviction decision one
+ * ss_decision_term(round, index, fields...). */
 #if defined(__CUDACC__)
 #define SS_HD __host__ __device__ __forceinline__
 #else
@@ -262,11 +263,22 @@ SS_HD uint64_t ss_round_fields(uint64_t round, uint64_t hdr, uint64_t mem, uint6
 #define SS_TAG_TIME  3u   /* unused since ss_round_fields */
 #define SS_TAG_GRANT 4u   /* unused since the grant terms above */
 #define SS_TAG_DONE  5u
-#define SS_TAG_EV0   6u   /* victim | action<<32     */
-#define SS_TAG_EV1   7u   /* saved | discarded<<32   */
-#define SS_TAG_EV2   8u   /* freed                   */
-#define SS_TAG_EV3   9u   /* f_t_before bits         */
-#define SS_TAG_EV4  10u   /* f_t_after bits          */
+#define SS_TAG_EV0   6u   /* unused since ss_decision_term */
+#define SS_TAG_EV1   7u
+#define SS_TAG_EV2   8u
+#define SS_TAG_EV3   9u
+#define SS_TAG_EV4  10u
+/* Eviction decision d of round r: one mixed (round, index) weight times a linear
+ * sum of its five fields w0 = victim | action<<32, w1 = saved | discarded<<32,
+ * w2 = freed, w3 / w4 = f_t before / after bits (odd field weights). */
+#define SS_DG_DEC 0x8CB92BA72F3D8DD7ull
+SS_HD uint64_t ss_decision_term(uint64_t round, uint32_t d, uint64_t w0, uint64_t w1, uint64_t w2, uint64_t w3,
+                                uint64_t w4) {
+    const uint64_t W = ss_mix64(((round << 24) ^ (uint64_t)d) * SS_DG_DEC) | 1u;
+    return W * (0xC2B2AE3D27D4EB4Full * (w0 ^ 0x165667B19E3779F9ull) + 0x27D4EB2F165667C5ull * (w1 ^ 0x85EBCA77C2B2AE63ull) +
+                0x9E3779B185EBCA87ull * (w2 ^ 0xFF51AFD7ED558CCDull) + 0xC4CEB9FE1A85EC53ull * (w3 ^ 0x62A9D9ED799705F5ull) +
+                0x4CF5AD432745937Full * (w4 ^ 0x1B873593CC9E2D51ull));
+}
 SS_HD uint64_t ss_hdr_word(uint32_t kind, uint32_t m, uint32_t c, uint32_t v) {
     return (uint64_t)kind | ((uint64_t)m << 8) | ((uint64_t)c << 24) | ((uint64_t)v << 40);
 }

@@ -466,11 +466,9 @@ static void record_round(osim* s, int kind, const int* g, int m, const int* c, i
         for (int k = 0; k < v; k++) {
             odecision* e = &s->dec[k];
             uint64_t fb, fa; memcpy(&fb, &e->ftb, 8); memcpy(&fa, &e->fta, 8);
-            d += ss_term(r, SS_TAG_EV0, k, (uint64_t)(uint32_t)e->victim | ((uint64_t)e->action << 32));
-            d += ss_term(r, SS_TAG_EV1, k, (uint64_t)(uint32_t)e->saved | ((uint64_t)(uint32_t)e->discarded << 32));
-            d += ss_term(r, SS_TAG_EV2, k, (uint64_t)e->freed);
-            d += ss_term(r, SS_TAG_EV3, k, fb);
-            d += ss_term(r, SS_TAG_EV4, k, fa);
+            d += ss_decision_term(r, (uint32_t)k, (uint64_t)(uint32_t)e->victim | ((uint64_t)e->action << 32),
+                                  (uint64_t)(uint32_t)e->saved | ((uint64_t)(uint32_t)e->discarded << 32),
+                                  (uint64_t)e->freed, fb, fa);
         }
         s->digest += d;
     }

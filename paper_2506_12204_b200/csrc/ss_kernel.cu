@@ -556,14 +556,9 @@ SS_EVICT_INLINE bool evict_one(const Env& E, Trace& T, Round& R, uint32_t kslot,
         }
         if (A.P.flags & SS_FLAG_DIGEST) {
             const unsigned long long r = (unsigned long long)T.rounds;
-            const unsigned long long w0 = (unsigned long long)v | ((unsigned long long)action << 32),
-                                     w1 = (unsigned long long)(uint32_t)saved | ((unsigned long long)(uint32_t)discarded << 32),
-                                     w2 = (unsigned long long)freed, w3 = dbits(ftb), w4 = dbits(fta);
-#pragma unroll 1
-            for (int f = 0; f < 5; f++) {  // one copy of the hash
-                const unsigned long long val = f == 0 ? w0 : (f == 1 ? w1 : (f == 2 ? w2 : (f == 3 ? w3 : w4)));
-                c.dpend += ss_term(r, SS_TAG_EV0 + (uint32_t)f, d, val);
-            }
+            c.dpend += ss_decision_term(r, (uint32_t)d, (unsigned long long)v | ((unsigned long long)action << 32),
+                                        (unsigned long long)(uint32_t)saved | ((unsigned long long)(uint32_t)discarded << 32),
+                                        (unsigned long long)freed, dbits(ftb), dbits(fta));
         }
         c.s_victims += 1;
     }

@@ -65,6 +65,15 @@ def round_mul(rnd):
     return ((2 * rnd + 1) * 0xA0761D6478BD642F) & M64
 
 
+def decision_term(rnd, d, w0, w1, w2, w3, w4):
+    # include/semsched_b200.h ss_decision_term
+    wt = mix64((((rnd << 24) ^ d) * 0x8CB92BA72F3D8DD7) & M64) | 1
+    v = (0xC2B2AE3D27D4EB4F * (w0 ^ 0x165667B19E3779F9) + 0x27D4EB2F165667C5 * (w1 ^ 0x85EBCA77C2B2AE63)
+         + 0x9E3779B185EBCA87 * (w2 ^ 0xFF51AFD7ED558CCD) + 0xC4CEB9FE1A85EC53 * (w3 ^ 0x62A9D9ED799705F5)
+         + 0x4CF5AD432745937F * (w4 ^ 0x1B873593CC9E2D51))
+    return (wt * v) & M64
+
+
 def round_fields(rnd, hdr, mem, tbits):
     # include/semsched_b200.h ss_round_fields
     v = (0xD1B54A32D192ED03 * (hdr ^ 0x5851F42D4C957F2D) + 0xAEF17502108EF2D9 * (mem ^ 0x14057B7EF767814F)
@@ -221,11 +230,8 @@ def run_case(name, cfg, arrivals_fn, keep_log):
         for j, e in enumerate(decs):
             act = 0 if e["prefill_action"] == "offload" else 1
             v = slot[e["victim"]]
-            d += term(k, 6, j, v | (act << 32))
-            d += term(k, 7, j, e["decode_saved"] | (e["decode_discarded"] << 32))
-            d += term(k, 8, j, e["freed_slots"])
-            d += term(k, 9, j, fbits(e["f_t_before"]))
-            d += term(k, 10, j, fbits(e["f_t_after"]))
+            d += decision_term(k, j, v | (act << 32), e["decode_saved"] | (e["decode_discarded"] << 32),
+                               e["freed_slots"], fbits(e["f_t_before"]), fbits(e["f_t_after"]))
             dl.append([v, act, e["decode_saved"], e["decode_discarded"], e["freed_slots"],
                        e["f_t_before"], e["f_t_after"]])
         digest = (digest + d) & M64
