@@ -78,6 +78,7 @@ struct Cold {
     int dense;        // no unservable request: pending index == slot
     int nuns, lost, anomalies, n;
     int dbg;  // SS_DEBUG_ANOM builds: general-path rounds run with anom set
+    Key dqk;  // stretch with queued decoding candidates: the best one's key (the last member must stay below it)
 };
 
 struct WarpSmem {
@@ -609,7 +610,10 @@ __device__ __noinline__ bool queue_has_stale(const KArgs* Ap, const WarpSmem* sm
 
 // ---- SS_DEBUG_TIMING builds: warp-cycles per kernel section -----------------
 #ifdef SS_DEBUG_TIMING
-__device__ unsigned long long g_dbg_cycles[24];
+constexpr int SS_DBG_SLOTS = 32;  // 16 section cycle counters + 16 event counters
+__device__ unsigned long long g_dbg_cycles[SS_DBG_SLOTS];
+constexpr int SS_DBG_TRACES = 8192;  // per-trace section cycles of the first traces (debug builds)
+__device__ unsigned long long g_dbg_trace[SS_DBG_TRACES][SS_DBG_SLOTS];
 #define SS_SECT(s_)                                                   \
     do {                                                              \
         const long long now_ = clock64();                             \
@@ -687,7 +691,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         return;
     const bool track_res = !noev;
 #ifdef SS_DEBUG_TIMING
-    unsigned long long dbg_acc[24] = {0};
+    unsigned long long dbg_acc[SS_DBG_SLOTS] = {0};
     long long dbg_t = clock64();
     int dbg_cur = 0;
 #endif
@@ -698,6 +702,14 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
         t = __shfl_sync(FULL, t, 0);
         if (uni(t >= A.in.n_traces)) break;
 
+#ifdef SS_DEBUG_TIMING
+        unsigned long long dbg_snap[SS_DBG_SLOTS];
+        for (int i = 0; i < SS_DBG_SLOTS; i++) dbg_snap[i] = dbg_acc[i];
+#endif
+#ifdef SS_DEBUG_TRACE_TIME
+        unsigned long long dbg_t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
+#endif
         Trace T;
         T.off = A.in.trace_offsets[t];
         const int n = (int)(A.in.trace_offsets[t + 1] - T.off);
@@ -845,7 +857,24 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 SS_SECT(5);
                 const int nc0 = T.nF < b ? T.nF : b;
                 const bool cdec = lane < nc0 && (sm->F[lane].aux & DEC_BIT);
-                if (!__any_sync(FULL, cdec)) {
+                // A queued decoding candidate (a preempted member) is eligible under p*'s
+                // stage rule (batching.py:73-88). With a full batch it changes nothing
+                // while it ranks after the last member: the merged top-b is the ongoing
+                // set and every candidate is pushed back with its unchanged key (a queued
+                // request's f_t does not move; the members' only decrease, so this holds
+                // for the whole stretch). A completion frees a slot the candidate would
+                // take: the stretch ends after that round (dq).
+                const unsigned dqm = __ballot_sync(FULL, cdec);
+                const bool dq = chunking && dqm != 0u;  // compile-time false in the per-round kernels
+                // (chunked kernels only: under the per-round kernel's heavy eviction such
+                // stretches mostly end before their first round, config D 91 -> 116 ms)
+                const bool blocks = cdec && !(chunking && T.nO == b && klt(sm->X[32 + (b - 1)], sm->F[lane]));
+                SS_DCOUNT(8, dq ? 1 : 0);
+                if (!__any_sync(FULL, blocks)) {
+                    if (dq) {  // the FRONT is sorted: its first decoding entry is the best one
+                        if (lane == 0) c.dqk = sm->F[__ffs(dqm) - 1];
+                        __syncwarp();
+                    }
                     const Key F0 = T.nF > 0 ? sm->F[0] : kinf();
                     int m = T.nO;
                     bool act = lane < m;
@@ -901,6 +930,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     bool need_setup = chunking;
                     if (!chunking) setup();
                     int k = 0;
+                    bool dq_exit = false;          // a completion freed a slot a queued decoding candidate takes
                     long long spool = 0, sgr = 0;  // live and granted requests summed over the rounds
                     int live_s = live;
                     for (;;) {
@@ -1062,6 +1092,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             T.nO = m;
                             live_s -= ncd;
                             if (uni(m == 0)) break;
+                            // a queued decoding candidate takes the freed slot next round: leave
+                            // after this round's key refresh and order check below
+                            dq_exit = dq;
                             if (chunking) need_setup = true;
                             else setup();
                         }
@@ -1133,6 +1166,10 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                     good = (rkp < rk) | ((n0p == n0) & (l0p == l0)) |
                                            (lin & linp & (f0 - f0p > thr) & (f1 - f1p > thr));
                                 }
+                                // a member past its predicted length (remainder clamped at 1) gains
+                                // f_t each round: the last member must then be checked against the
+                                // best queued decoding candidate round by round
+                                if (dq && lane == m - 1) good &= lin;
                                 // only the pairs (and p*) the screen cannot settle run the exact loop
                                 const unsigned sus = __ballot_sync(FULL, act & !good);
                                 const int s_lo = __ffs(sus) - 1;
@@ -1154,6 +1191,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                                 // key order (rank, f_t, tie) without packing: f_t > 0 orders like its bits
                                 if (i == 0) pk = klt_nb(make_key<POL>(rk, ft, tie, 0, true), F0);
                                 else if (i > i_lo) ok &= (prk < rk) | ((prk == rk) & ((pft < ft) | ((pft == ft) & (ptie < tie))));
+                                if (dq && i == m - 1) ok &= klt_nb(make_key<POL>(rk, ft, tie, 0, true), c.dqk);
                                 pft = ft;
                                 prk = rk;
                                 ptie = tie;
@@ -1245,6 +1283,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             __syncwarp();
                         }
                         if (reord) break;  // positions moved: the next stretch recomputes the grant terms
+                        // the next round's batch would take a queued decoding candidate
+                        if (dq && (dq_exit || __any_sync(FULL, (lane == m - 1) & !klt_nb(okey, c.dqk)))) break;
                     }
                     if (uni(T.rounds >= round_cap)) set_status(T, SS_TRACE_ROUND_CAP);
                     if (logging && uni(c.logpos > c.logcap)) set_status(T, SS_TRACE_LOG_OVERFLOW);
@@ -1940,22 +1980,41 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 st->anomalies = c.anomalies;
 #ifdef SS_DEBUG_ANOM
                 st->_pad = c.dbg;
+#elif defined(SS_DEBUG_TRACE_TIME)  // dev builds: start and duration of the trace (ns, globaltimer)
+                unsigned long long dbg_t1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t1));
+                st->_pad = (int)(dbg_t1 - dbg_t0);
+                st->sum_pool = (long long)dbg_t0;
+                {
+                    unsigned smid;
+                    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                    st->sum_victims = (long long)smid;
+                }
 #else
                 st->_pad = 0;
 #endif
+#ifndef SS_DEBUG_TRACE_TIME
                 st->sum_pool = c.s_pool;
+#endif
                 st->sum_granted = c.s_granted;
+#ifndef SS_DEBUG_TRACE_TIME
                 st->sum_victims = c.s_victims;
+#endif
                 st->sum_resident_evict = c.s_res;
                 st->final_clock = T.clock;
             }
         }
+#ifdef SS_DEBUG_TIMING
+        SS_SECT(0);
+        if (lane == 0 && t < SS_DBG_TRACES)
+            for (int i = 0; i < SS_DBG_SLOTS; i++) g_dbg_trace[t][i] = dbg_acc[i] - dbg_snap[i];
+#endif
         __syncwarp();
     }
 #ifdef SS_DEBUG_TIMING
     SS_SECT(0);
     if (lane == 0)
-        for (int i = 0; i < 24; i++) atomicAdd(&g_dbg_cycles[i], dbg_acc[i]);
+        for (int i = 0; i < SS_DBG_SLOTS; i++) atomicAdd(&g_dbg_cycles[i], dbg_acc[i]);
 #endif
 }
 
@@ -2095,10 +2154,15 @@ int sched_launches(int policy) { return policy == SS_POLICY_SEMANTIC ? 3 : 1; }
 
 #ifdef SS_DEBUG_TIMING
 // debug builds only (not part of include/semsched_b200.h): read and clear the section counters
+extern "C" int ss_debug_trace_cycles(unsigned long long* out, int n) {
+    cudaDeviceSynchronize();
+    if (n > ss::SS_DBG_TRACES) n = ss::SS_DBG_TRACES;
+    return cudaMemcpyFromSymbol(out, ss::g_dbg_trace, sizeof(unsigned long long) * ss::SS_DBG_SLOTS * (size_t)n) == cudaSuccess ? 0 : -1;
+}
 extern "C" int ss_debug_cycles(unsigned long long* out) {
     cudaDeviceSynchronize();
-    if (cudaMemcpyFromSymbol(out, ss::g_dbg_cycles, sizeof(unsigned long long) * 24) != cudaSuccess) return -1;
-    unsigned long long z[24] = {0};
+    if (cudaMemcpyFromSymbol(out, ss::g_dbg_cycles, sizeof(unsigned long long) * ss::SS_DBG_SLOTS) != cudaSuccess) return -1;
+    unsigned long long z[ss::SS_DBG_SLOTS] = {0};
     return cudaMemcpyToSymbol(ss::g_dbg_cycles, z, sizeof(z)) == cudaSuccess ? 0 : -1;
 }
 #endif

@@ -15,7 +15,7 @@ batch = bench.native_batch(W, wl, np.arange(T), pinned=False)
 force = {"auto": 0, "chunked": A.SS_FLAG_FORCE_CHUNKED, "perround": A.SS_FLAG_FORCE_PERROUND}[os.environ.get("SS_BENCH_VARIANT", "auto")]
 prm = make_params(get_profile(wl["profile"]), 16, wl["capacity"], levels=wl["levels"], flags=A.SS_FLAG_DIGEST | force)
 lib = native.lib()
-buf = (C.c_ulonglong * 24)()
+buf = (C.c_ulonglong * 32)()
 native.run_host(prm, batch)  # warm-up
 lib.ss_debug_cycles(buf)
 res = native.run_host(prm, batch)
@@ -34,4 +34,5 @@ if c[5]: print(f"  refills {c[5]}, cycles per refill {v[15] / c[5]:.0f}")
 if c[4]: print(f"  evict_one calls {c[4]}, cycles per call {v[14] / c[4]:.0f}")
 if c[0]: print(f"  cycles/chunk {v[2] / c[0]:.0f}, per chunk round {v[2] / max(c[1], 1):.0f}, order screen settled {100 * c[6] / c[0]:.1f}% of chunks, exact loop {c[7] / c[0]:.2f} members per chunk")
 if c[2]: print(f"  cycles per per-round fast round {v[1] / c[2]:.0f}")
+print(f"  stretch entries with a queued decoding candidate below the full batch: {c[8]}")
 if c[3]: print(f"  cycles per general round (composition .. queue rebuild) {sum(v[i] for i in (3, 8, 9, 10, 11, 12, 13)) / c[3]:.0f}")
