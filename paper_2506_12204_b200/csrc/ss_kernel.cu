@@ -54,6 +54,11 @@
 namespace ss {
 
 constexpr int kChunkUnroll = SS_CHUNK_UNROLL;
+#ifndef SS_DQ_PERROUND
+#define SS_DQ_PERROUND 0  // stretches behind queued decoding candidates in the per-round kernels too
+                          // (measured: config D 91.5 -> 104 ms, its stretches end before they pay)
+#endif
+constexpr bool kDqPerRound = SS_DQ_PERROUND != 0;
 #ifndef SS_CHAIN_STEP
 #define SS_CHAIN_STEP 4  // clock-chain rounds per uniform loop step in a chunk (8: 3% slower, code size)
 #endif
@@ -865,10 +870,10 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 // for the whole stretch). A completion frees a slot the candidate would
                 // take: the stretch ends after that round (dq).
                 const unsigned dqm = __ballot_sync(FULL, cdec);
-                const bool dq = chunking && dqm != 0u;  // compile-time false in the per-round kernels
+                const bool dq = (chunking || kDqPerRound) && dqm != 0u;  // compile-time false in the per-round kernels
                 // (chunked kernels only: under the per-round kernel's heavy eviction such
                 // stretches mostly end before their first round, config D 91 -> 116 ms)
-                const bool blocks = cdec && !(chunking && T.nO == b && klt(sm->X[32 + (b - 1)], sm->F[lane]));
+                const bool blocks = cdec && !((chunking || kDqPerRound) && T.nO == b && klt(sm->X[32 + (b - 1)], sm->F[lane]));
                 SS_DCOUNT(8, dq ? 1 : 0);
                 if (!__any_sync(FULL, blocks)) {
                     if (dq) {  // the FRONT is sorted: its first decoding entry is the best one
