@@ -18,13 +18,26 @@ from collections import defaultdict
 
 # kernel line ranges (ss_kernel.cu) -> section name; edit to the file's layout
 SECTIONS = [
-    ("trace init", 659, 772), ("admission/refill/anom", 773, 848), ("stretch entry+setup+vote", 849, 954),
-    ("per-round fast body", 955, 1074), ("chunk: clock chain", 1075, 1113), ("chunk: order screen", 1114, 1150),
-    ("chunk: exact loop", 1151, 1168), ("chunk: stop vote", 1169, 1179), ("chunk: digest", 1180, 1191),
-    ("chunk: log", 1192, 1209), ("chunk: commit", 1210, 1227), ("stretch order/exit", 1228, 1272),
-    ("g: composition", 1273, 1462), ("g: KV admission", 1463, 1625), ("g: batch duration", 1626, 1666),
-    ("g: progress", 1667, 1817), ("g: record+digest", 1818, 1864), ("g: ongoing rebuild", 1865, 1906),
-    ("g: queue rebuild", 1907, 1931), ("outputs/stats", 1932, 1965),
+    ("trace init", 663, 785),
+    ("admission/refill/anom", 786, 861),
+    ("stretch entry+setup+vote", 862, 986),
+    ("per-round fast body", 987, 1108),
+    ("chunk: clock chain", 1109, 1146),
+    ("chunk: order screen", 1147, 1187),
+    ("chunk: exact loop", 1188, 1206),
+    ("chunk: stop vote", 1207, 1217),
+    ("chunk: digest", 1218, 1228),
+    ("chunk: log", 1229, 1247),
+    ("chunk: commit", 1248, 1265),
+    ("stretch order/exit", 1266, 1312),
+    ("g: composition", 1313, 1502),
+    ("g: KV admission", 1503, 1665),
+    ("g: batch duration", 1666, 1706),
+    ("g: progress", 1707, 1857),
+    ("g: record+digest", 1858, 1904),
+    ("g: ongoing rebuild", 1905, 1946),
+    ("g: queue rebuild", 1947, 1971),
+    ("outputs/stats", 1972, 2032),
 ]
 
 
