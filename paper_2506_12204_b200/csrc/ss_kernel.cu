@@ -875,6 +875,9 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                 // stretches mostly end before their first round, config D 91 -> 116 ms)
                 const bool blocks = cdec && !((chunking || kDqPerRound) && T.nO == b && klt(sm->X[32 + (b - 1)], sm->F[lane]));
                 SS_DCOUNT(8, dq ? 1 : 0);
+#ifdef SS_DEBUG_D
+                SS_DCOUNT(12, __any_sync(FULL, blocks) ? 1 : 0);
+#endif
                 if (!__any_sync(FULL, blocks)) {
                     if (dq) {  // the FRONT is sorted: its first decoding entry is the best one
                         if (lane == 0) c.dqk = sm->F[__ffs(dqm) - 1];
@@ -951,6 +954,11 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         const bool pdec = act & klt_nb(okey, F0);
                         bool cround = false;  // a member completes in this round
                         if (__all_sync(FULL, (left <= 0) | adm | capx | !pdec)) {
+#ifdef SS_DEBUG_TIMING
+                            SS_DCOUNT(9, uni(adm) ? 1 : 0);
+                            SS_DCOUNT(10, (!uni(adm) && !__any_sync(FULL, pdec)) ? 1 : 0);
+                            SS_DCOUNT(11, uni((left <= 0) & !adm & !capx) && __any_sync(FULL, pdec) ? 1 : 0);
+#endif
                             // completing members are handled here when that is the only reason
                             if (!uni((left <= 0) & !adm & !capx) || !__any_sync(FULL, pdec)) break;
                             cround = true;
@@ -960,7 +968,13 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             long long e = (long long)m_mid(mem) - (long long)mem.dec;
                             long long dem = e > 1 ? e : 1;
                             if (dem + lane > cap) dem = 1;
-                            if (__any_sync(FULL, act && dem + lane + T.used > cap)) break;  // eviction
+                            if (__any_sync(FULL, act && dem + lane + T.used > cap)) {
+#ifdef SS_DEBUG_D
+                                SS_DCOUNT(13, 1);
+                                SS_DCOUNT(14, k == 0 ? 1 : 0);
+#endif
+                                break;  // eviction
+                            }
                         }
                         // ---- a chunk of up to 32 rounds, one lane per round ----------
                         // Within a stretch nothing but the clock is a serial chain: round
@@ -1211,6 +1225,14 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             const unsigned stop = __ballot_sync(FULL, lim | adm_j) |
                                                   (__ballot_sync(FULL, !(pk & ok)) << 1);
                             const int Lx = stop ? __ffs(stop) - 1 : 32;  // >= 1: round 0 passed the vote
+#if defined(SS_DEBUG_TIMING) && !defined(SS_DEBUG_D)
+                            {
+                                const unsigned s_lim = __ballot_sync(FULL, lim), s_adm = __ballot_sync(FULL, adm_j);
+                                SS_DCOUNT(12, Lx == L ? 1 : 0);
+                                SS_DCOUNT(13, (Lx < L && ((s_adm >> Lx) & 1u) && !((s_lim >> Lx) & 1u)) ? 1 : 0);
+                                SS_DCOUNT(14, (Lx < L && !((s_adm >> Lx) & 1u) && !((s_lim >> Lx) & 1u)) ? 1 : 0);
+                            }
+#endif
                             SS_DCOUNT(0, 1);
                             SS_DCOUNT(1, Lx);
                             const bool runj = lane < Lx;
@@ -1287,6 +1309,7 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             }
                             __syncwarp();
                         }
+                        SS_DCOUNT(15, reord ? 1 : 0);
                         if (reord) break;  // positions moved: the next stretch recomputes the grant terms
                         // the next round's batch would take a queued decoding candidate
                         if (dq && (dq_exit || __any_sync(FULL, (lane == m - 1) & !klt_nb(okey, c.dqk)))) break;

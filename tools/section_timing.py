@@ -35,4 +35,9 @@ if c[4]: print(f"  evict_one calls {c[4]}, cycles per call {v[14] / c[4]:.0f}")
 if c[0]: print(f"  cycles/chunk {v[2] / c[0]:.0f}, per chunk round {v[2] / max(c[1], 1):.0f}, order screen settled {100 * c[6] / c[0]:.1f}% of chunks, exact loop {c[7] / c[0]:.2f} members per chunk")
 if c[2]: print(f"  cycles per per-round fast round {v[1] / c[2]:.0f}")
 print(f"  stretch entries with a queued decoding candidate below the full batch: {c[8]}")
+print(f"  stretch vote exits: admission {c[9]}, p* queued {c[10]}, completion rounds {c[11]}; reorders {c[15]}")
+if os.environ.get("SS_DEBUG_D"):
+    print(f"  stretch entry refused (queued decoding candidate) {c[12]}; eviction breaks {c[13]}, of which before any round {c[14]}")
+else:
+    print(f"  chunk ends: at L (completion / 32) {c[12]}, admission {c[13]}, order / p* {c[14]}")
 if c[3]: print(f"  cycles per general round (composition .. queue rebuild) {sum(v[i] for i in (3, 8, 9, 10, 11, 12, 13)) / c[3]:.0f}")
