@@ -310,7 +310,7 @@ int ss_run_traces(const ss_params* params, const ss_trace_batch* batch,
 /* Same, with every pointer in `batch` and `out` on the HOST (pinned or
  * pageable). Copies in, runs, copies out, synchronises. This is the
  * reference-facing plugin call (host buffers in, host buffers out).
- * Batches of >= 2,048 traces run as up to 4 slices of consecutive traces on
+ * Batches of >= 1,024 traces run as up to 8 equal slices of consecutive traces on
  * library-owned streams (which first wait for `stream`): uploads, kernels and
  * downloads of different slices overlap. Pinned buffers give full overlap.
  * `kernel_ms` then reports the span from the first slice's prepass to the

@@ -2,6 +2,7 @@
 // launch, optional host staging. No torch types cross this boundary.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -57,10 +58,10 @@ int validate(const ss_params* p, const ss_trace_batch* b, const ss_outputs* o) {
 }
 
 #ifndef SS_SLICE_TRACES
-#define SS_SLICE_TRACES 1024  // ss_run_traces_host pipelines batches of >= 2 slices of this size
+#define SS_SLICE_TRACES 512  // ss_run_traces_host pipelines batches of >= 2 slices of this size
 #endif
 #ifndef SS_MAX_SLICES
-#define SS_MAX_SLICES 4
+#define SS_MAX_SLICES 8
 #endif
 struct HostStage {
     std::mutex mu;
@@ -222,13 +223,12 @@ int ss_run_traces_host(const ss_params* params, const ss_trace_batch* hb, const 
     // slice's finished warps free. Every slice is an independent ss_run_traces.
     int S = (int)(T / SLICE_TRACES);
     S = S < 1 ? 1 : (S > SS_MAX_SLICES ? SS_MAX_SLICES : S);
+    if (const char* e = getenv("SS_HOST_SLICES")) {  // dev: slice-count experiments
+        const int v = atoi(e);
+        if (v >= 1 && v <= SS_MAX_SLICES) S = v;
+    }
     int32_t t0s[SS_MAX_SLICES + 1];
     for (int s = 0; s <= S; s++) t0s[s] = (int32_t)((int64_t)T * s / S);
-    if (S == 4) {  // small first / last slices: compute starts sooner, the last download is shorter
-        t0s[1] = T / 8;
-        t0s[2] = T / 2;
-        t0s[3] = T - T / 8;
-    }
     size_t in_b = 2 * a16((size_t)(n > 0 ? n : 1) * 8) + 4 * a16((size_t)(n > 0 ? n : 1) * 4) +
                   2 * a16((size_t)(n > 0 ? n : 1));
     const size_t nn = (size_t)(n > 0 ? n : 1);
