@@ -65,8 +65,9 @@ WORKLOADS = {
                    "seed=s)), s = 0..65535), block-partitioned over the GPUs, b=16, ample KV, a100_qwen7b",
               traces=65536, requests=2000, capacity=10**9, profile="a100_qwen7b", levels=5, scaling="strong"),
 }
-# traces of the bounded CPU sample per step (C port, all host threads): ~10-15 s of CPU work
-CPU_SAMPLE = {"A": 1, "B": 256, "D": 128, "E": 128}
+# traces of the bounded CPU sample per step (C port, all host threads): ~2-3 s per run on 16
+# threads, i.e. ~30-45 s of CPU work per run; cpu_baseline = 1 warm-up + 2 timed runs
+CPU_SAMPLE = {"A": 1, "B": 1024, "D": 512, "E": 256}
 # traces of the Python-reference sample (one multiprocessing pool run)
 PY_SAMPLE = {"A": 1, "B": 16, "D": 16, "E": 16}
 
