@@ -1084,7 +1084,8 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         sgr += m;
                         if (cround) {
                             // resident list upkeep for the completed (engine.py:414-421)
-                            unsigned cm = cdm;
+                            unsigned cm = track_res ? cdm : 0u;
+                            if (!track_res) T.nR -= ncd;  // no resident list in the no-eviction kernels
                             __syncwarp();
                             while (cm) {
                                 const int q = __ffs(cm) - 1;
