@@ -401,3 +401,29 @@ def test_gpu_unservable_duplicate_pinned(native, variant):
     assert int(cpu.stats["status"][0]) == A.SS_TRACE_REF_ERROR
     assert int(gpu.stats["status"][0]) == A.SS_TRACE_LIVELOCK
     assert int(gpu.stats["rounds"][0]) == int(cpu.stats["rounds"][0])
+
+
+@pytest.mark.parametrize("b", [4, 8, 16, 32])
+@variants
+def test_gpu_queued_decoding_candidates_with_length_errors(native, b, variant):
+    """Stretches (and chunks) that run while preempted decoding requests wait
+    behind a full batch: with predictor length errors members
+    decode past their predicted length, their remainder clamps at 1 and their
+    f_t grows, so the last member can overtake a queued candidate mid-stretch;
+    bursty arrivals (up to 12 per tick) keep preempting members. Every request
+    record, round count and digest against the oracle, ample and tight budgets."""
+    from oracle_binding import run_oracle
+    from paper_2506_12204_b200.costs import get_profile
+    from paper_2506_12204_b200.predictors import PredictorConfig
+    from paper_2506_12204_b200.results import make_params
+    from paper_2506_12204_b200.tracegen import generate_batch
+    from paper_2506_12204_b200.workload import WorkloadSpec
+
+    spec = WorkloadSpec(total_requests=400, levels=4, concurrent=12, gap_s=0.1)
+    batch = generate_batch(spec, np.arange(900 + b, 900 + b + 64),
+                           PredictorConfig(length_error=0.5, urgency_error=0.1), threads=4)
+    for cap in (10**9, 4000):
+        p = lambda f=0: make_params(get_profile("a100_qwen7b"), b, cap, levels=4, flags=A.SS_FLAG_DIGEST | f)
+        gpu = native.run_host(p(VARIANTS[variant]), batch)
+        cpu = run_oracle(p(), batch, threads=8)
+        assert _compare_with_oracle(gpu, cpu, batch) >= batch.n_traces // 2
