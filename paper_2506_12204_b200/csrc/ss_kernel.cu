@@ -613,6 +613,177 @@ __device__ __noinline__ bool queue_has_stale(const KArgs* Ap, const WarpSmem* sm
     return __any_sync(FULL, st);
 }
 
+
+// A general round whose batch holds duplicate copies of one request (stale heap
+// entries after a lost eviction decision): the copies execute one
+// by one (engine.py:351-421), each seeing the previous copy's effect. Out of
+// line: only stale-entry rounds of the evicting kernels come here.
+struct DupOut {
+    long long used;
+    int nR, err;
+    bool done;
+};
+__device__ __noinline__ DupOut progress_dups(const KArgs* Ap, long long off, uint32_t G, double clock, double end,
+                                             long long cap, long long used, int nR, MemS mem) {
+    const KArgs& A = *Ap;
+    const ss_profile& P = A.P.profile;
+    const int lane = threadIdx.x & 31;
+    bool done = false;
+    int err_out = 0;
+                    // duplicate copies of a request: execute copies one by one,
+                    // each seeing the previous copy's effect
+                    unsigned gm = G;
+                    while (uni(gm != 0u)) {
+                        const int k = __ffs(gm) - 1;
+                        gm &= gm - 1;
+                        int err = 0, dn = 0, nres = 0;
+                        long long alloc = 0, rel = 0;
+                        if (lane == k) {
+                            const long long g = off + mem.slot;
+                            const Dyn d = DYN(A)[g];
+                            uint32_t dec = d.dec, fl = d.flg;
+                            if ((fl & F_STAGE) == ST_DONE) {
+                                err = 1;  // transition(PREFILLING) from COMPLETED
+                            } else {
+                                if (!(fl & F_FIRST)) {
+                                    A.out.req.first_scheduled[g] = clock;
+                                    fl |= F_FIRST;
+                                }
+                                if ((fl & F_STAGE) == ST_DEC) {
+                                    alloc = 1;
+                                    dec += 1;
+                                } else {
+                                    const long long pfn = (fl & F_PF) ? (long long)m_prompt(mem) : 0;
+                                    alloc = pfn + dec + ((long long)m_prompt(mem) - pfn);
+                                    fl = (fl & ~F_STAGE) | ST_DEC | F_PF;
+                                    nres = 1;
+                                }
+                                fl &= ~F_GRANT;
+                                double ft;
+                                if (dec >= m_tout(mem)) {
+                                    dn = 1;
+                                    rel = (long long)m_prompt(mem) + dec;
+                                    A.out.req.finish_time[g] = end;
+                                    ft = 0.0;
+                                    fl = (fl & ~F_STAGE) | ST_DONE;
+                                } else {
+                                    ft = remaining_time(m_prompt(mem), m_mid(mem), m_prompt(mem), dec, 0, P);
+                                }
+                                store_dyn(A, g, ft, dec, fl);
+                            }
+                        }
+                        err = __shfl_sync(FULL, err, k);
+                        dn = __shfl_sync(FULL, dn, k);
+                        nres = __shfl_sync(FULL, nres, k);
+                        alloc = __shfl_sync(FULL, alloc, k);
+                        rel = __shfl_sync(FULL, rel, k);
+                        const uint32_t s = __shfl_sync(FULL, mem.slot, k);
+                        if (uni(err || alloc > cap - used)) {
+                            err_out = 1;
+                            break;
+                        }
+                        used += alloc;
+                        if (lane == k) done = dn != 0;
+                        if (lane == 0 && nres) {
+                            A.w.R[off + nR] = s;
+                            A.w.rpos[off + s] = (uint32_t)nR;
+                        }
+                        if (nres) nR += 1;
+                        __syncwarp();
+                        if (dn) {
+                            if (lane == 0) {
+                                const uint32_t ri = A.w.rpos[off + s];
+                                const uint32_t last = A.w.R[off + nR - 1];
+                                A.w.R[off + ri] = last;
+                                A.w.rpos[off + last] = ri;
+                            }
+                            nR -= 1;
+                            used -= rel;
+                        }
+                        __syncwarp();
+                    }
+    DupOut o;
+    o.used = used;
+    o.nR = nR;
+    o.err = err_out;
+    o.done = done;
+    return o;
+}
+
+
+// Merged positions of candidates and ongoing copies while stale heap entries may
+// exist: a stable sort of (candidates + ongoing) by current key;
+// equal keys are copies of one request, ordered by pool position. Out of line.
+__device__ __noinline__ int2 rank_general(WarpSmem* sm, int nc, int nO, unsigned cmask, bool c_elig, bool has_o, Key ck,
+                                          Key okey) {
+    const int lane = threadIdx.x & 31;
+    int cnt_c = 0, cnt_o = 0;
+    if (c_elig) sm->X[lane] = ck;
+    if (has_o) sm->X[32 + lane] = okey;
+    __syncwarp();
+    for (int k = 0; uni(k < nc); k++) {
+        if (!((cmask >> k) & 1u)) continue;
+        Key x = sm->X[k];
+        if (c_elig && (klt(x, ck) || (keq(x, ck) && k < lane))) cnt_c++;
+        if (has_o && (klt(x, okey) || keq(x, okey))) cnt_o++;
+    }
+    for (int k = 0; uni(k < nO); k++) {
+        Key x = sm->X[32 + k];
+        if (c_elig && klt(x, ck)) cnt_c++;
+        if (has_o && (klt(x, okey) || (keq(x, okey) && k < lane))) cnt_o++;
+    }
+    return make_int2(cnt_c, cnt_o);
+}
+
+
+// Push-backs of a general round while stale heap entries may exist (DESIGN.md
+// §5): candidates not selected whose stored key is stale are re-queued with
+// their current key (heaps.py insert after pop); pushed-back ongoing copies are
+// re-queued, and one whose request is still queued is the reference's
+// DuplicateRequestError (heaps.py:49-51). Out of line.
+struct PushOut {
+    unsigned rm;
+    int nins, err;
+};
+__device__ __noinline__ PushOut push_back_stale(const KArgs* Ap, WarpSmem* sm, long long off, int nins, bool has_c,
+                                                bool c_sel, Key ck, bool pushed, Key okey) {
+    const KArgs& A = *Ap;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    PushOut o;
+    o.err = 0;
+    const bool refresh = has_c && !c_sel && !keq(ck, sm->F[lane]);
+    const unsigned rm2 = __ballot_sync(FULL, refresh);
+    o.rm = rm2;
+    if (refresh) {
+        const uint32_t s = ck.aux & SLOT_MASK;
+        INS(A)[off + nins + __popc(rm2 & lt)] = ck;
+        *FLG(A, off + s) = *FLG(A, off + s) | F_INS;
+    }
+    nins += __popc(rm2);
+    __syncwarp();
+    unsigned pm = __ballot_sync(FULL, pushed);
+    while (pm) {
+        const int k = __ffs(pm) - 1;
+        pm &= pm - 1;
+        const uint32_t s = sm->OM[k].slot;
+        const uint32_t f = *FLG(A, off + s);
+        if (uni(f & F_Q)) {
+            o.err = 1;
+            break;
+        }
+        const Key kk = kshfl(okey, k);
+        if (lane == 0) {
+            *FLG(A, off + s) = f | F_Q | F_INS;
+            INS(A)[off + nins] = kk;
+        }
+        nins += 1;
+        __syncwarp();
+    }
+    o.nins = nins;
+    return o;
+}
+
 // ---- SS_DEBUG_TIMING builds: warp-cycles per kernel section -----------------
 #ifdef SS_DEBUG_TIMING
 constexpr int SS_DBG_SLOTS = 32;  // 16 section cycle counters + 16 event counters
@@ -1413,22 +1584,10 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                     }
                 }
             } else {
-                // general: stable sort of (candidates + ongoing) by current key;
-                // equal keys are copies of one request, ordered by pool position
-                if (c_elig) sm->X[lane] = ck;
-                if (has_o) sm->X[32 + lane] = okey;
-                __syncwarp();
-                for (int k = 0; uni(k < nc); k++) {
-                    if (!((cmask >> k) & 1u)) continue;
-                    Key x = sm->X[k];
-                    if (c_elig && (klt(x, ck) || (keq(x, ck) && k < lane))) cnt_c++;
-                    if (has_o && (klt(x, okey) || keq(x, okey))) cnt_o++;
-                }
-                for (int k = 0; uni(k < T.nO); k++) {
-                    Key x = sm->X[32 + k];
-                    if (c_elig && klt(x, ck)) cnt_c++;
-                    if (has_o && (klt(x, okey) || (keq(x, okey) && k < lane))) cnt_o++;
-                }
+                // general: stable sort of (candidates + ongoing) by current key (out of line)
+                const int2 cc = rank_general(sm, nc, T.nO, cmask, c_elig, has_o, ck, okey);
+                cnt_c = cc.x;
+                cnt_o = cc.y;
             }
             const int elig = __popc(cmask) + T.nO;
             const int m = elig < b ? elig : b;
@@ -1455,38 +1614,12 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
             }
             if (!direct && has_o && cnt_o < m) sm->M[cnt_o] = sm->OM[lane];
             if (anom_ok && uni(anom)) {
-                // candidates not selected are pushed back with their current key;
-                // a stale stored key is replaced (heaps.py insert after pop)
-                const bool refresh = has_c && !c_sel && !keq(ck, sm->F[lane]);
-                const unsigned rm2 = __ballot_sync(FULL, refresh);
-                R.rmF |= (unsigned long long)rm2;
-                if (refresh) {
-                    const uint32_t s = ck.aux & SLOT_MASK;
-                    INS(A)[T.off + T.nins + __popc(rm2 & lt)] = ck;
-                    *FLG(A, T.off + s) = *FLG(A, T.off + s) | F_INS;
-                }
-                T.nins += __popc(rm2);
-                __syncwarp();
-                // pushed-back ongoing copies: inserting an id already queued is a
-                // DuplicateRequestError in the reference (heaps.py:49-51)
-                unsigned pm = __ballot_sync(FULL, has_o && cnt_o >= m);
-                while (pm) {
-                    const int k = __ffs(pm) - 1;
-                    pm &= pm - 1;
-                    const uint32_t s = sm->OM[k].slot;
-                    const uint32_t f = *FLG(A, T.off + s);
-                    if (uni(f & F_Q)) {
-                        set_status(T, SS_TRACE_REF_ERROR);
-                        break;
-                    }
-                    const Key kk = kshfl(okey, k);
-                    if (lane == 0) {
-                        *FLG(A, T.off + s) = f | F_Q | F_INS;
-                        INS(A)[T.off + T.nins] = kk;
-                    }
-                    T.nins += 1;
-                    __syncwarp();
-                }
+                // candidates not selected are pushed back with their current key; a stale
+                // stored key is replaced; pushed-back ongoing copies (out of line)
+                const PushOut po = push_back_stale(&A, sm, T.off, T.nins, has_c, c_sel, ck, has_o && cnt_o >= m, okey);
+                R.rmF |= (unsigned long long)po.rm;
+                T.nins = po.nins;
+                if (po.err) set_status(T, SS_TRACE_REF_ERROR);
             } else {
                 const bool pushed = has_o && cnt_o >= m;
                 const unsigned pm = __ballot_sync(FULL, pushed);
@@ -1795,77 +1928,14 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                         }
                     }
                 } else {
-                    // duplicate copies of a request: execute copies one by one,
-                    // each seeing the previous copy's effect
-                    unsigned gm = R.G;
-                    while (uni(gm && T.status == SS_TRACE_OK)) {
-                        const int k = __ffs(gm) - 1;
-                        gm &= gm - 1;
-                        int err = 0, dn = 0, nres = 0;
-                        long long alloc = 0, rel = 0;
-                        if (lane == k) {
-                            const long long g = T.off + mem.slot;
-                            const Dyn d = DYN(A)[g];
-                            uint32_t dec = d.dec, fl = d.flg;
-                            if ((fl & F_STAGE) == ST_DONE) {
-                                err = 1;  // transition(PREFILLING) from COMPLETED
-                            } else {
-                                if (!(fl & F_FIRST)) {
-                                    A.out.req.first_scheduled[g] = T.clock;
-                                    fl |= F_FIRST;
-                                }
-                                if ((fl & F_STAGE) == ST_DEC) {
-                                    alloc = 1;
-                                    dec += 1;
-                                } else {
-                                    const long long pfn = (fl & F_PF) ? (long long)m_prompt(mem) : 0;
-                                    alloc = pfn + dec + ((long long)m_prompt(mem) - pfn);
-                                    fl = (fl & ~F_STAGE) | ST_DEC | F_PF;
-                                    nres = 1;
-                                }
-                                fl &= ~F_GRANT;
-                                double ft;
-                                if (dec >= m_tout(mem)) {
-                                    dn = 1;
-                                    rel = (long long)m_prompt(mem) + dec;
-                                    A.out.req.finish_time[g] = end;
-                                    ft = 0.0;
-                                    fl = (fl & ~F_STAGE) | ST_DONE;
-                                } else {
-                                    ft = remaining_time(m_prompt(mem), m_mid(mem), m_prompt(mem), dec, 0, P);
-                                }
-                                store_dyn(A, g, ft, dec, fl);
-                            }
-                        }
-                        err = __shfl_sync(FULL, err, k);
-                        dn = __shfl_sync(FULL, dn, k);
-                        nres = __shfl_sync(FULL, nres, k);
-                        alloc = __shfl_sync(FULL, alloc, k);
-                        rel = __shfl_sync(FULL, rel, k);
-                        const uint32_t s = __shfl_sync(FULL, mem.slot, k);
-                        if (uni(err || alloc > cap - T.used)) {
-                            set_status(T, SS_TRACE_REF_ERROR);
-                            break;
-                        }
-                        T.used += alloc;
-                        if (lane == k) done = dn != 0;
-                        if (lane == 0 && nres) {
-                            A.w.R[T.off + T.nR] = s;
-                            A.w.rpos[T.off + s] = (uint32_t)T.nR;
-                        }
-                        if (nres) T.nR += 1;
-                        __syncwarp();
-                        if (dn) {
-                            if (lane == 0) {
-                                const uint32_t ri = A.w.rpos[T.off + s];
-                                const uint32_t last = A.w.R[T.off + T.nR - 1];
-                                A.w.R[T.off + ri] = last;
-                                A.w.rpos[T.off + last] = ri;
-                            }
-                            T.nR -= 1;
-                            T.used -= rel;
-                        }
-                        __syncwarp();
+                    // duplicate copies of a request (stale heap entries): out of
+                    // line, the hot general round carries none of this code
+                    {
+                        const DupOut o = progress_dups(&A, T.off, R.G, T.clock, end, cap, T.used, T.nR, mem);
+                        T.used = o.used;
+                        T.nR = o.nR;
+                        if (o.err) set_status(T, SS_TRACE_REF_ERROR);
+                        done = o.done;
                     }
                     if (uni(T.status != SS_TRACE_OK)) {
                         T.rounds += 1;
