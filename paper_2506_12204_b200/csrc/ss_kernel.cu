@@ -1300,10 +1300,15 @@ __global__ void __launch_bounds__(32 * WPB, SS_MINB) sched_kernel(const __grid_c
                             const double pj =
                                 ss::add(0.0, decode_step_time((long long)(nmax + (unsigned)lane), 1, P));
                             double clk = T.clock;
+                            // the rounds' durations broadcast from shared memory (one load per round
+                            // instead of two shuffles of the double)
+                            double* pjs = chain + 32;
+                            pjs[lane] = pj;
+                            __syncwarp();
                             for (int q0 = 0; uni(q0 < L); q0 += kChainStep) {
 #pragma unroll
                                 for (int q = 0; q < kChainStep; q++) {
-                                    clk = ss::add(clk, __shfl_sync(FULL, pj, q0 + q));
+                                    clk = ss::add(clk, pjs[q0 + q]);
                                     if (lane == 0) chain[q0 + q] = clk;
                                 }
                             }
