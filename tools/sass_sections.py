@@ -18,26 +18,26 @@ from collections import defaultdict
 
 # kernel line ranges (ss_kernel.cu) -> section name; edit to the file's layout
 SECTIONS = [
-    ("trace init", 663, 785),
-    ("admission/refill/anom", 786, 861),
-    ("stretch entry+setup+vote", 862, 986),
-    ("per-round fast body", 987, 1108),
-    ("chunk: clock chain", 1109, 1146),
-    ("chunk: order screen", 1147, 1187),
-    ("chunk: exact loop", 1188, 1206),
-    ("chunk: stop vote", 1207, 1217),
-    ("chunk: digest", 1218, 1228),
-    ("chunk: log", 1229, 1247),
-    ("chunk: commit", 1248, 1265),
-    ("stretch order/exit", 1266, 1312),
-    ("g: composition", 1313, 1502),
-    ("g: KV admission", 1503, 1665),
-    ("g: batch duration", 1666, 1706),
-    ("g: progress", 1707, 1857),
-    ("g: record+digest", 1858, 1904),
-    ("g: ongoing rebuild", 1905, 1946),
-    ("g: queue rebuild", 1947, 1971),
-    ("outputs/stats", 1972, 2032),
+    ("trace init", 834, 956),
+    ("admission/refill/anom", 957, 1032),
+    ("stretch entry+setup+vote", 1033, 1171),
+    ("per-round fast body", 1172, 1294),
+    ("chunk: clock chain", 1295, 1337),
+    ("chunk: order screen", 1338, 1378),
+    ("chunk: exact loop", 1379, 1397),
+    ("chunk: stop vote", 1398, 1416),
+    ("chunk: digest", 1417, 1427),
+    ("chunk: log", 1428, 1446),
+    ("chunk: commit", 1447, 1464),
+    ("stretch order/exit", 1465, 1512),
+    ("g: composition", 1513, 1664),
+    ("g: KV admission", 1665, 1827),
+    ("g: batch duration", 1828, 1868),
+    ("g: progress", 1869, 1956),
+    ("g: record+digest", 1957, 2003),
+    ("g: ongoing rebuild", 2004, 2045),
+    ("g: queue rebuild", 2046, 2070),
+    ("outputs/stats", 2071, 2131),
 ]
 
 
