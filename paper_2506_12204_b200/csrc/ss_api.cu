@@ -115,6 +115,10 @@ int ss_kernel_config(const ss_params* params, int32_t n_traces, int* blocks, int
     int maxb = ss::sched_max_blocks(params ? params->policy : 0, &sms);
     if (maxb <= 0) return fail(SS_ERR_UNSUPPORTED, "kernel not available");
     int need = (n_traces + ss::WPB - 1) / ss::WPB;
+    if (const char* e = getenv("SS_BLOCKS_PER_SM")) {  // dev: occupancy experiments
+        int per = atoi(e);
+        if (per > 0 && per * sms < maxb) maxb = per * sms;
+    }
     if (blocks) *blocks = need < maxb ? (need > 0 ? need : 1) : maxb;
     if (warps_per_block) *warps_per_block = ss::WPB;
     if (smem_bytes_per_block) *smem_bytes_per_block = ss::sched_smem_bytes();
