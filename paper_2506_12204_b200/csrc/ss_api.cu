@@ -119,6 +119,10 @@ int ss_kernel_config(const ss_params* params, int32_t n_traces, int* blocks, int
         int per = atoi(e);
         if (per > 0 && per * sms < maxb) maxb = per * sms;
     }
+    if (const char* e = getenv("SS_MAX_BLOCKS")) {  // dev: wave-balance experiments
+        int mb = atoi(e);
+        if (mb > 0 && mb < maxb) maxb = mb;
+    }
     if (blocks) *blocks = need < maxb ? (need > 0 ? need : 1) : maxb;
     if (warps_per_block) *warps_per_block = ss::WPB;
     if (smem_bytes_per_block) *smem_bytes_per_block = ss::sched_smem_bytes();
