@@ -47,6 +47,9 @@
 #ifndef SS_CHUNK_UNROLL
 #define SS_CHUNK_UNROLL 1  // unroll of the chunk's member loop
 #endif
+#ifndef SS_REFILL_AHEAD
+#define SS_REFILL_AHEAD 2  // chunks of 32 BACK keys in flight while refill merges one
+#endif
 #ifndef SS_CHUNK_MIN
 #define SS_CHUNK_MIN 4  // shortest static bound for which a stretch runs a lane-per-round chunk
 #endif
@@ -63,6 +66,7 @@ constexpr bool kDqPerRound = SS_DQ_PERROUND != 0;
 #define SS_CHAIN_STEP 4  // clock-chain rounds per uniform loop step in a chunk (8: 3% slower, code size)
 #endif
 constexpr int kChainStep = SS_CHAIN_STEP;
+constexpr int kRefillAhead = SS_REFILL_AHEAD;
 
 // a request's state as one unit: static record, dynamic record, slot
 struct __align__(16) MemS {
@@ -322,12 +326,16 @@ __device__ __noinline__ int4 refill(const KArgs* Ap, WarpSmem* sm, long long off
     const int lane = threadIdx.x & 31;
     QState T{off, nF, nB};
     Key S = kinf();  // running top-32, ascending across lanes
-    // the next chunk's load is issued before the current chunk is merged
-    Key xn = lane < T.nB ? BK(A)[T.off + lane] : kinf();
+    // the next kRefillAhead chunks' loads are in flight while the current one is merged
+    Key xq[kRefillAhead];
+#pragma unroll
+    for (int d = 0; d < kRefillAhead; d++) xq[d] = 32 * d + lane < T.nB ? BK(A)[T.off + 32 * d + lane] : kinf();
     for (int base = 0; uni(base < T.nB); base += 32) {
-        Key x = xn;
-        const int in = base + 32 + lane;
-        xn = in < T.nB ? BK(A)[T.off + in] : kinf();
+        Key x = xq[0];
+#pragma unroll
+        for (int d = 0; d + 1 < kRefillAhead; d++) xq[d] = xq[d + 1];
+        const int in = base + 32 * kRefillAhead + lane;
+        xq[kRefillAhead - 1] = in < T.nB ? BK(A)[T.off + in] : kinf();
         Key smax = kshfl(S, 31);
         unsigned qm = __ballot_sync(FULL, klt(x, smax));
         if (!qm) continue;
@@ -380,13 +388,17 @@ __device__ __noinline__ int4 refill(const KArgs* Ap, WarpSmem* sm, long long off
         // compact the BACK, dropping the selected keys (all <= thr)
         const unsigned lt = lanemask_lt();
         int w = 0;
-        // survivors land at or below their own index, never in the chunk loaded ahead
-        Key xn2 = lane < T.nB ? BK(A)[T.off + lane] : kinf();
+        // survivors land at or below their own index, never in the chunks loaded ahead
+        Key yq[kRefillAhead];
+#pragma unroll
+        for (int d = 0; d < kRefillAhead; d++) yq[d] = 32 * d + lane < T.nB ? BK(A)[T.off + 32 * d + lane] : kinf();
         for (int base = 0; uni(base < T.nB); base += 32) {
             int i = base + lane;
-            const Key x = xn2;
-            const int in = base + 32 + lane;
-            xn2 = in < T.nB ? BK(A)[T.off + in] : kinf();
+            const Key x = yq[0];
+#pragma unroll
+            for (int d = 0; d + 1 < kRefillAhead; d++) yq[d] = yq[d + 1];
+            const int in = base + 32 * kRefillAhead + lane;
+            yq[kRefillAhead - 1] = in < T.nB ? BK(A)[T.off + in] : kinf();
             const bool keep = i < T.nB && klt(thr, x);
             unsigned km = __ballot_sync(FULL, keep);
             __syncwarp();
